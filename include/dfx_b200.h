@@ -1,0 +1,197 @@
+/*
+ * dfx_b200.h — C-ABI of the B200-native MotionDeltaCNN sparse frame-difference
+ * inference path (drop-in for the reference "deltaflux" engine path).
+ *
+ * Every entry point here replaces one piece of the reference's public surface
+ * for the hot path (paths relative to /root/reference/proj):
+ *
+ *   dfx_engine_create        dflx::DeltaEngine::DeltaEngine(spec, cfg)   include/deltaflux/engine.hpp:47,
+ *                            src/engine.cpp:7-15 (validate() at src/network.cpp:46-254)
+ *   dfx_engine_destroy       ~DeltaEngine
+ *   dfx_engine_run_frame     DeltaEngine::run_frame(frame, h, roi)      engine.hpp:51, engine.cpp:184-287;
+ *                            python: deltaflux._core.DeltaEngine.run_frame  bindings/py_bindings.cpp:103-121
+ *   dfx_engine_submit_frame  (async variant of run_frame for throughput; no reference counterpart)
+ *   dfx_engine_sync          (completes submitted frames)
+ *   dfx_engine_reset         DeltaEngine::reset()                      engine.hpp:55, engine.cpp:93-108
+ *   dfx_engine_input_mask    FrameResult::input_mask                    engine.hpp:38
+ *   dfx_engine_layer_flops   FrameResult::flops (FlopReport::layers)    tensor.hpp:105-123
+ *   dfx_engine_read_state    truncation_state()/maxpool_state()/input_state() buffers
+ *                            engine.hpp:64-67 (SphericalBuffer::storage, tile_grid.hpp:116)
+ *   dfx_engine_read_packet   the per-layer DeltaPacket the observer sees  engine.hpp:69-70, engine.cpp:239,279
+ *   dfx_engine_read_ledger   DeltaEngine::ledger()                     engine.hpp:64 (TileLedger, buffer_manager.hpp:13-88)
+ *   dfx_wrap_tile            dflx::wrap_tile                            tile_grid.hpp:37-40
+ *
+ * Conventions: every call returns 0 on success and a nonzero dfx_status on
+ * failure; dfx_last_error() returns a thread-local message (C++ exceptions
+ * cannot cross this boundary — the reference throws dflx::Error /
+ * ValidationError, common.hpp:14-32; the Python mirror re-raises
+ * DeltafluxError). Tensors crossing the boundary are host float32 in the
+ * reference's CHW layout; spherical-buffer readbacks are in the reference's
+ * wrapped CHW planar layout (c, floor_mod(gy, PH), floor_mod(gx, PW)).
+ */
+#ifndef DFX_B200_H
+#define DFX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Layer kinds, same set and meaning as dflx::LayerKind (network.hpp:11). */
+typedef enum {
+    DFX_CONV = 0,
+    DFX_RELU = 1,
+    DFX_TRUNCATE = 2,
+    DFX_MAXPOOL = 3,
+    DFX_AVGPOOL = 4,
+    DFX_UPSAMPLE = 5,
+    DFX_BATCHNORM = 6,
+    DFX_ADD = 7,
+    DFX_OUTPUT = 8
+} dfx_layer_kind;
+
+typedef enum {
+    DFX_OK = 0,
+    DFX_ERR = 1,            /* dflx::Error */
+    DFX_ERR_VALIDATION = 2, /* dflx::ValidationError */
+    DFX_ERR_IO = 3,         /* dflx::IoError */
+    DFX_ERR_CUDA = 4        /* device failure (no reference counterpart) */
+} dfx_status;
+
+/* One layer, mirroring dflx::LayerDef (network.hpp:15-27). Pointers are only
+ * read during dfx_engine_create. */
+typedef struct {
+    const char* name;
+    int kind;               /* dfx_layer_kind */
+    const char* input0;     /* "input" = network input */
+    const char* input1;     /* Add only, else NULL */
+    /* Conv (ConvParams, tensor.hpp:58-87): weights O-I-Kh-Kw fp32 */
+    int in_channels;
+    int out_channels;
+    int kernel;             /* square, odd */
+    int stride;
+    int padding;
+    const float* weights;
+    const float* bias;      /* NULL = no bias */
+    /* MaxPool / AvgPool */
+    int pool_k;
+    int pool_stride;
+    /* Upsample */
+    int factor;
+    /* BatchNorm */
+    int bn_channels;
+    const float* bn_scale;
+    const float* bn_shift;
+    /* Relu / Truncate */
+    int has_threshold;
+    float threshold;
+    int truncate_enabled;
+} dfx_layer_desc;
+
+typedef struct {
+    int in_channels;
+    int num_layers;
+    const dfx_layer_desc* layers;
+} dfx_net_desc;
+
+/* Convolution arithmetic for the sparse DeltaConv kernel. */
+typedef enum {
+    DFX_CONV_TF32X3 = 0, /* tcgen05 kind::tf32, 3-pass split (fp32-grade), default */
+    DFX_CONV_EXACT = 1   /* CUDA-core fp32, reference summation order: bit-exact */
+} dfx_conv_mode;
+
+/* dflx::EngineConfig (engine.hpp:10-21) plus the device-only knob conv_mode. */
+typedef struct {
+    int tile_size;
+    int grid_rows;
+    int grid_cols;
+    float input_threshold;
+    float default_threshold;
+    int override_net_thresholds;
+    int mask_dilation;
+    int roi_enabled;
+    int noise_suppression;
+    int padded_convolutions;
+    int conv_mode;          /* dfx_conv_mode */
+} dfx_engine_config;
+
+/* Scalar part of dflx::FrameResult / FrameEvents (engine.hpp:23-39). */
+typedef struct {
+    int64_t frame_index;
+    int64_t origin_tx;
+    int64_t origin_ty;
+    int tiles_h;
+    int tiles_w;
+    int fresh;
+    int evicted;
+    int reset;
+    int64_t dropped_pixels;
+    double update_rate;
+    uint64_t conv_flops;
+    uint64_t dense_flops;
+    int out_channels;
+    int out_height;
+    int out_width;
+} dfx_frame_info;
+
+typedef struct dfx_engine dfx_engine;
+
+/* Buffer selectors for dfx_engine_read_state. */
+enum { DFX_STATE_ACC = 0, DFX_STATE_TRUNC = 1, DFX_STATE_PREV = 2 };
+
+const char* dfx_last_error(void);
+void dfx_default_config(dfx_engine_config* cfg);
+
+int dfx_engine_create(const dfx_net_desc* net, const dfx_engine_config* cfg, int device,
+                      dfx_engine** out);
+int dfx_engine_destroy(dfx_engine* e);
+
+/* Synchronous frame: host CHW frame (c x h x w fp32), 3x3 row-major
+ * homography, optional 1 x h x w ROI map. On return `info` is filled and the
+ * densified output (out_channels x out_height x out_width, CHW) is copied to
+ * `out` when out_cap (in floats) is large enough. */
+int dfx_engine_run_frame(dfx_engine* e, const float* frame, int c, int h, int w, const float* h9,
+                         const float* roi, dfx_frame_info* info, float* out, size_t out_cap);
+
+/* Asynchronous frame on device-resident input (frame_dev: device pointer,
+ * CHW). Launches the whole frame on the engine's CUDA stream and returns
+ * without waiting; results of the last frame are readable after
+ * dfx_engine_sync. */
+int dfx_engine_submit_frame(dfx_engine* e, const float* frame_dev, int c, int h, int w,
+                            const float* h9);
+int dfx_engine_sync(dfx_engine* e, dfx_frame_info* info);
+
+int dfx_engine_reset(dfx_engine* e);
+
+/* Device pointer of the last densified output (CHW), valid until the next frame. */
+int dfx_engine_output_device(dfx_engine* e, const float** ptr, int* c, int* h, int* w);
+
+int dfx_engine_input_mask(dfx_engine* e, uint8_t* out, size_t cap, int* tiles_h, int* tiles_w);
+int dfx_engine_num_layers(dfx_engine* e);
+int dfx_engine_layer_flops(dfx_engine* e, int layer, uint64_t* flops, uint64_t* dense_flops);
+int dfx_engine_grid(dfx_engine* e, int* rows, int* cols);
+
+/* Spherical buffer readback in the reference's wrapped CHW layout. layer is a
+ * layer name or "input". On success *c, *h, *w give the buffer shape. */
+int dfx_engine_read_state(dfx_engine* e, const char* layer, int which, float* out, size_t cap,
+                          int* c, int* h, int* w);
+/* Last frame's output packet of `layer` ("input" = gated input packet) as the
+ * reference's dense grown CHW tensor with zeros in unmasked tiles. */
+int dfx_engine_read_packet(dfx_engine* e, const char* layer, float* out, size_t cap, int* c,
+                           int* gh, int* gw, int* halo, uint8_t* mask, size_t mask_cap);
+int dfx_engine_read_ledger(dfx_engine* e, int* used, int64_t* ty, int64_t* tx, uint8_t* covered,
+                           size_t cap);
+
+/* Device work counters of the last frame (for the roofline): number of
+ * launches of each kernel family, and algorithmic bytes per family. */
+int dfx_engine_kernel_count(dfx_engine* e);
+
+void dfx_wrap_tile(int64_t tx, int64_t ty, int rows, int cols, int* row, int* col);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DFX_B200_H */

@@ -1,0 +1,367 @@
+// ORACLE / TEST INFRASTRUCTURE ONLY — never linked into or called by the
+// product path. Only tests/, __graft_entry__.smoke() and bench.py's
+// cpu_baseline / --impl reference leg may load the library built from this
+// file (oracle/_ref/libdfxref.so).
+//
+// A thin C-ABI over the UNMODIFIED reference engine (dflx::DeltaEngine,
+// /root/reference/proj/src, compiled from the sources where they lie by
+// oracle/Makefile). It exposes the same entry points as include/dfx_b200.h
+// under the dfr_ prefix, so the parity tests drive the reference, the C
+// restatement (oracle/dfx_oracle.c, dfo_ prefix) and the CUDA product
+// (dfx_ prefix) through one interface.
+
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "deltaflux/engine.hpp"
+#include "deltaflux/synth.hpp"
+#include "dfx_b200.h"
+
+using namespace dflx;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail_with(const std::exception& e) {
+    g_err = e.what();
+    if (dynamic_cast<const ValidationError*>(&e)) return DFX_ERR_VALIDATION;
+    if (dynamic_cast<const IoError*>(&e)) return DFX_ERR_IO;
+    return DFX_ERR;
+}
+
+struct StoredPacket {
+    int c = 0, gh = 0, gw = 0, halo = 0, th = 0, tw = 0;
+    std::vector<float> data;
+    std::vector<uint8_t> mask;
+};
+
+struct RefEngine {
+    std::unique_ptr<DeltaEngine> eng;
+    std::map<std::string, StoredPacket> packets;
+    FrameResult last;
+    bool have_last = false;
+};
+
+NetworkSpec spec_from(const dfx_net_desc* d) {
+    NetworkSpec s;
+    s.in_channels = d->in_channels;
+    for (int i = 0; i < d->num_layers; ++i) {
+        const dfx_layer_desc& L = d->layers[i];
+        LayerDef l;
+        l.name = L.name ? L.name : "";
+        l.kind = static_cast<LayerKind>(L.kind);
+        if (L.input0) l.inputs.push_back(L.input0);
+        if (L.input1) l.inputs.push_back(L.input1);
+        if (l.kind == LayerKind::Conv) {
+            l.conv.in_channels = L.in_channels;
+            l.conv.out_channels = L.out_channels;
+            l.conv.kernel_h = l.conv.kernel_w = L.kernel;
+            l.conv.stride = L.stride;
+            l.conv.padding = L.padding;
+            const size_t n = static_cast<size_t>(L.out_channels) * L.in_channels * L.kernel * L.kernel;
+            l.conv.weights.assign(L.weights, L.weights + n);
+            if (L.bias) l.conv.bias.assign(L.bias, L.bias + L.out_channels);
+        }
+        l.pool_k = L.pool_k;
+        l.pool_stride = L.pool_stride;
+        l.factor = L.factor;
+        if (l.kind == LayerKind::BatchNorm) {
+            l.bn_scale.assign(L.bn_scale, L.bn_scale + L.bn_channels);
+            l.bn_shift.assign(L.bn_shift, L.bn_shift + L.bn_channels);
+        }
+        if (L.has_threshold) l.threshold = L.threshold;
+        l.truncate_enabled = L.truncate_enabled != 0;
+        s.layers.push_back(std::move(l));
+    }
+    return s;
+}
+
+EngineConfig cfg_from(const dfx_engine_config* c) {
+    EngineConfig e;
+    e.tile_size = c->tile_size;
+    e.grid_rows = c->grid_rows;
+    e.grid_cols = c->grid_cols;
+    e.input_threshold = c->input_threshold;
+    e.default_threshold = c->default_threshold;
+    e.override_net_thresholds = c->override_net_thresholds != 0;
+    e.mask_dilation = c->mask_dilation;
+    e.roi_enabled = c->roi_enabled != 0;
+    e.noise_suppression = c->noise_suppression != 0;
+    e.padded_convolutions = c->padded_convolutions != 0;
+    return e;
+}
+
+void fill_info(const FrameResult& r, dfx_frame_info* info) {
+    info->frame_index = r.events.frame_index;
+    info->origin_tx = r.place.origin.tx;
+    info->origin_ty = r.place.origin.ty;
+    info->tiles_h = r.place.tiles_h;
+    info->tiles_w = r.place.tiles_w;
+    info->fresh = r.events.fresh;
+    info->evicted = r.events.evicted;
+    info->reset = r.events.reset ? 1 : 0;
+    info->dropped_pixels = r.events.dropped_pixels;
+    info->update_rate = r.update_rate;
+    info->conv_flops = r.flops.total;
+    info->dense_flops = r.flops.dense_total;
+    info->out_channels = r.output.channels;
+    info->out_height = r.output.height;
+    info->out_width = r.output.width;
+}
+
+const SphericalBuffer* pick_buffer(const DeltaEngine& e, const std::string& layer, int which) {
+    if (layer == "input") {
+        if (which == DFX_STATE_ACC) return &e.input_state().accumulated;
+        if (which == DFX_STATE_TRUNC) return &e.input_state().truncated;
+        return nullptr;
+    }
+    if (const TruncationState* t = e.truncation_state(layer)) {
+        if (which == DFX_STATE_ACC) return &t->accumulated;
+        if (which == DFX_STATE_TRUNC) return &t->truncated;
+        return nullptr;
+    }
+    if (const MaxPoolState* p = e.maxpool_state(layer)) {
+        if (which == DFX_STATE_ACC) return &p->accumulated;
+        if (which == DFX_STATE_PREV) return &p->prev_out;
+        return nullptr;
+    }
+    return nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dfr_last_error(void) { return g_err.c_str(); }
+
+int dfr_create(const dfx_net_desc* net, const dfx_engine_config* cfg, void** out) {
+    try {
+        auto* r = new RefEngine;
+        r->eng = std::make_unique<DeltaEngine>(spec_from(net), cfg_from(cfg));
+        RefEngine* rp = r;
+        r->eng->set_observer([rp](const std::string& name, const DeltaPacket& p) {
+            StoredPacket& s = rp->packets[name];
+            s.c = p.channels();
+            s.gh = p.grown_h();
+            s.gw = p.grown_w();
+            s.halo = p.halo;
+            s.th = p.place.tiles_h;
+            s.tw = p.place.tiles_w;
+            s.data = p.delta.data;
+            s.mask = p.mask.bits;
+        });
+        *out = r;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_with(e);
+    }
+}
+
+void dfr_destroy(void* e) { delete static_cast<RefEngine*>(e); }
+
+int dfr_run_frame(void* ev, const float* frame, int c, int h, int w, const float* h9,
+                  const float* roi, dfx_frame_info* info, float* out, size_t out_cap) {
+    try {
+        auto* r = static_cast<RefEngine*>(ev);
+        Tensor f(c, h, w);
+        std::memcpy(f.data.data(), frame, f.size() * sizeof(float));
+        Homography H;
+        std::memcpy(H.m.data(), h9, 9 * sizeof(float));
+        Tensor roi_t;
+        if (roi) {
+            roi_t = Tensor(1, h, w);
+            std::memcpy(roi_t.data.data(), roi, roi_t.size() * sizeof(float));
+        }
+        r->packets.clear();
+        r->last = r->eng->run_frame(f, H, roi ? &roi_t : nullptr);
+        r->have_last = true;
+        fill_info(r->last, info);
+        if (out && out_cap >= r->last.output.size())
+            std::memcpy(out, r->last.output.data.data(), r->last.output.size() * sizeof(float));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_with(e);
+    }
+}
+
+int dfr_reset(void* ev) {
+    try {
+        static_cast<RefEngine*>(ev)->eng->reset();
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_with(e);
+    }
+}
+
+int dfr_input_mask(void* ev, uint8_t* out, size_t cap, int* th, int* tw) {
+    auto* r = static_cast<RefEngine*>(ev);
+    if (!r->have_last) {
+        g_err = "no frame";
+        return DFX_ERR;
+    }
+    const TileMask& m = r->last.input_mask;
+    *th = m.tiles_h;
+    *tw = m.tiles_w;
+    if (cap < m.bits.size()) {
+        g_err = "mask buffer too small";
+        return DFX_ERR;
+    }
+    std::memcpy(out, m.bits.data(), m.bits.size());
+    return 0;
+}
+
+int dfr_layer_flops(void* ev, const char* name, uint64_t* flops, uint64_t* dense) {
+    auto* r = static_cast<RefEngine*>(ev);
+    for (const auto& l : r->last.flops.layers)
+        if (l.name == name) {
+            *flops = l.flops;
+            *dense = l.dense_flops;
+            return 0;
+        }
+    *flops = 0;
+    *dense = 0;
+    return 0;
+}
+
+int dfr_grid(void* ev, int* rows, int* cols) {
+    auto* r = static_cast<RefEngine*>(ev);
+    const GridSpec g = r->eng->input_grid();
+    *rows = g.rows;
+    *cols = g.cols;
+    return 0;
+}
+
+int dfr_read_state(void* ev, const char* layer, int which, float* out, size_t cap, int* c, int* h,
+                   int* w) {
+    auto* r = static_cast<RefEngine*>(ev);
+    const SphericalBuffer* b = pick_buffer(*r->eng, layer, which);
+    if (!b) {
+        g_err = std::string("no state buffer for layer ") + layer;
+        return DFX_ERR;
+    }
+    *c = b->channels();
+    *h = b->spec().pixel_h();
+    *w = b->spec().pixel_w();
+    if (out) {
+        if (cap < b->storage().size()) {
+            g_err = "state buffer too small";
+            return DFX_ERR;
+        }
+        std::memcpy(out, b->storage().data(), b->storage().size() * sizeof(float));
+    }
+    return 0;
+}
+
+int dfr_read_packet(void* ev, const char* layer, float* out, size_t cap, int* c, int* gh, int* gw,
+                    int* halo, uint8_t* mask, size_t mask_cap) {
+    auto* r = static_cast<RefEngine*>(ev);
+    auto it = r->packets.find(layer);
+    if (it == r->packets.end()) {
+        g_err = std::string("no packet for layer ") + layer;
+        return DFX_ERR;
+    }
+    const StoredPacket& s = it->second;
+    *c = s.c;
+    *gh = s.gh;
+    *gw = s.gw;
+    *halo = s.halo;
+    if (out) {
+        if (cap < s.data.size() || mask_cap < s.mask.size()) {
+            g_err = "packet buffer too small";
+            return DFX_ERR;
+        }
+        std::memcpy(out, s.data.data(), s.data.size() * sizeof(float));
+        std::memcpy(mask, s.mask.data(), s.mask.size());
+    }
+    return 0;
+}
+
+int dfr_read_ledger(void* ev, int* used, int64_t* ty, int64_t* tx, uint8_t* covered, size_t cap) {
+    auto* r = static_cast<RefEngine*>(ev);
+    const TileLedger& L = r->eng->ledger();
+    const size_t n = static_cast<size_t>(L.rows()) * L.cols();
+    if (cap < n) {
+        g_err = "ledger buffer too small";
+        return DFX_ERR;
+    }
+    for (int rr = 0; rr < L.rows(); ++rr)
+        for (int cc = 0; cc < L.cols(); ++cc) {
+            const auto& s = L.slot_local(rr, cc);
+            const size_t i = static_cast<size_t>(rr) * L.cols() + cc;
+            used[i] = s.used ? 1 : 0;
+            ty[i] = s.coord.ty;
+            tx[i] = s.coord.tx;
+            covered[i] = s.covered ? 1 : 0;
+        }
+    return 0;
+}
+
+// The reference's seeded texture generator (synth.cpp:5-30), used by the
+// bench / tests to make identical inputs for every implementation.
+int dfr_synth_texture(int c, int h, int w, uint32_t seed, float* out) {
+    try {
+        std::mt19937 rng(seed);
+        const Tensor t = synth_texture(c, h, w, rng);
+        std::memcpy(out, t.data.data(), t.size() * sizeof(float));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_with(e);
+    }
+}
+
+// CPU baseline: `streams` independent engines (one per host thread, the
+// reference's "one engine instance per video stream"), each
+// running `frames` frames of its own sequence. Frame f of stream s is
+// frames_data[s][f] (c x h x w) with homography h9s[s][f]. Per-frame wall
+// seconds are written to secs[s * frames + f].
+int dfr_run_streams(const dfx_net_desc* net, const dfx_engine_config* cfg, int streams, int frames,
+                    int c, int h, int w, const float* frames_data, const float* h9s, double* secs,
+                    uint64_t* flops) {
+    try {
+        const NetworkSpec spec = spec_from(net);
+        const EngineConfig ec = cfg_from(cfg);
+        std::vector<std::thread> th;
+        std::vector<std::string> errs(streams);
+        for (int s = 0; s < streams; ++s) {
+            th.emplace_back([&, s] {
+                try {
+                    DeltaEngine eng(spec, ec);
+                    const size_t fsz = static_cast<size_t>(c) * h * w;
+                    for (int f = 0; f < frames; ++f) {
+                        Tensor t(c, h, w);
+                        std::memcpy(t.data.data(), frames_data + (static_cast<size_t>(s) * frames + f) * fsz,
+                                    fsz * sizeof(float));
+                        Homography H;
+                        std::memcpy(H.m.data(), h9s + (static_cast<size_t>(s) * frames + f) * 9,
+                                    9 * sizeof(float));
+                        const auto t0 = std::chrono::steady_clock::now();
+                        const FrameResult r = eng.run_frame(t, H);
+                        const auto t1 = std::chrono::steady_clock::now();
+                        secs[static_cast<size_t>(s) * frames + f] =
+                            std::chrono::duration<double>(t1 - t0).count();
+                        if (flops) flops[static_cast<size_t>(s) * frames + f] = r.flops.total;
+                    }
+                } catch (const std::exception& e) {
+                    errs[s] = e.what();
+                }
+            });
+        }
+        for (auto& t : th) t.join();
+        for (const auto& e : errs)
+            if (!e.empty()) {
+                g_err = e;
+                return DFX_ERR;
+            }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_with(e);
+    }
+}
+
+}  // extern "C"
