@@ -173,7 +173,6 @@ def load_library():
         ("num_layers", C.c_int, [C.c_void_p]),
         ("layer_flops", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         ("kernel_count", C.c_int, [C.c_void_p]),
-        ("stats", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int]),
     ]:
         fn = getattr(lib, f"dfx_engine_{name}")
         fn.restype = res

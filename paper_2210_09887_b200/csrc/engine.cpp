@@ -1,0 +1,925 @@
+// B200 delta engine: host orchestrator + C-ABI (include/dfx_b200.h).
+//
+// Mirrors dflx::DeltaEngine (reference include/deltaflux/engine.hpp:45-91,
+// src/engine.cpp:7-287): per frame it factors the homography, snaps the frame
+// to the tile grid, plans the ledger on the host (integer work), uploads one
+// per-frame parameter block, and launches the device pipeline
+//   claims reset/bias -> input stage -> per layer (conv | truncate | pool |
+//   linear ops) -> densify
+// on one CUDA stream. Every per-frame value the kernels need is read on device
+// from the uploaded FrameDev block, so the launch sequence is shape-stable.
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "dfx_b200.h"
+#include "host.hpp"
+#include "kernels.hpp"
+
+namespace dfx {
+
+namespace {
+
+thread_local std::string g_err;
+
+#define CUDA_CHECK(x)                                                                                  \
+    do {                                                                                               \
+        cudaError_t _e = (x);                                                                          \
+        if (_e != cudaSuccess) fail(std::string("CUDA: ") + cudaGetErrorString(_e) + " at " #x, DFX_ERR_CUDA); \
+    } while (0)
+
+int64_t fdiv(int64_t a, int64_t n) { return floor_div64(a, n); }
+int64_t cdiv(int64_t a, int64_t n) { return ceil_div64(a, n); }
+
+template <typename T>
+struct DevArr {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) {
+            cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+            if (e != cudaSuccess) fail(std::string("CUDA malloc: ") + cudaGetErrorString(e), DFX_ERR_CUDA);
+        }
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevArr() { release(); }
+    DevArr() = default;
+    DevArr(const DevArr&) = delete;
+    DevArr& operator=(const DevArr&) = delete;
+    DevArr(DevArr&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+    DevArr& operator=(DevArr&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p, n = o.n, o.p = nullptr, o.n = 0;
+        }
+        return *this;
+    }
+};
+
+// ---- homography (alignment.cpp:5-56), host double / float exactly as the reference
+void hom_compose(const float* m, const float* inner, float* r) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 3; ++k) s += (double)m[i * 3 + k] * inner[k * 3 + j];
+            r[i * 3 + j] = (float)s;
+        }
+    if (r[8] != 0.0f && r[8] != 1.0f) {
+        const float d = r[8];
+        for (int i = 0; i < 8; ++i) r[i] /= d;
+        r[8] /= r[8];
+    }
+}
+void hom_inverse(const float* a, float* r) {
+    const double d = (double)a[0] * ((double)a[4] * a[8] - (double)a[5] * a[7]) -
+                     (double)a[1] * ((double)a[3] * a[8] - (double)a[5] * a[6]) +
+                     (double)a[2] * ((double)a[3] * a[7] - (double)a[4] * a[6]);
+    check(std::fabs(d) > 1e-9, "homography: singular matrix");
+    const double inv = 1.0 / d;
+    r[0] = (float)(((double)a[4] * a[8] - (double)a[5] * a[7]) * inv);
+    r[1] = (float)(((double)a[2] * a[7] - (double)a[1] * a[8]) * inv);
+    r[2] = (float)(((double)a[1] * a[5] - (double)a[2] * a[4]) * inv);
+    r[3] = (float)(((double)a[5] * a[6] - (double)a[3] * a[8]) * inv);
+    r[4] = (float)(((double)a[0] * a[8] - (double)a[2] * a[6]) * inv);
+    r[5] = (float)(((double)a[2] * a[3] - (double)a[0] * a[5]) * inv);
+    r[6] = (float)(((double)a[3] * a[7] - (double)a[4] * a[6]) * inv);
+    r[7] = (float)(((double)a[1] * a[6] - (double)a[0] * a[7]) * inv);
+    r[8] = (float)(((double)a[0] * a[4] - (double)a[1] * a[3]) * inv);
+}
+bool hom_int_translation(const float* m, int64_t* dx, int64_t* dy) {
+    auto is = [](float v, float t) { return std::fabs(v - t) < 1e-6f; };
+    if (!is(m[0], 1) || !is(m[1], 0) || !is(m[3], 0) || !is(m[4], 1) || !is(m[6], 0) || !is(m[7], 0) || !is(m[8], 1))
+        return false;
+    const float tx = m[2], ty = m[5];
+    if (std::fabs(tx - std::round(tx)) > 1e-4f || std::fabs(ty - std::round(ty)) > 1e-4f) return false;
+    *dx = (int64_t)std::llround(tx);
+    *dy = (int64_t)std::llround(ty);
+    return true;
+}
+
+int64_t overlap(int64_t a0, int64_t a1, int64_t b0, int64_t b1) {
+    const int64_t lo = std::max(a0, b0), hi = std::min(a1, b1);
+    return hi > lo ? hi - lo : 0;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ engine
+class Engine {
+  public:
+    Engine(const dfx_net_desc* d, const dfx_engine_config* cfg, int device);
+    ~Engine();
+
+    void run_frame(const float* frame, int c, int h, int w, const float* h9, const float* roi, dfx_frame_info* info,
+                   float* out, size_t cap);
+    void submit(const float* frame_dev, int c, int h, int w, const float* h9);
+    void sync(dfx_frame_info* info);
+    void reset();
+
+    // readbacks
+    void read_state(const std::string& layer, int which, float* out, size_t cap, int* c, int* h, int* w);
+    void read_packet(const std::string& layer, float* out, size_t cap, int* c, int* gh, int* gw, int* halo,
+                     uint8_t* mask, size_t mask_cap);
+    void read_ledger(int* used, int64_t* ty, int64_t* tx, uint8_t* covered, size_t cap) const;
+    void input_mask(uint8_t* out, size_t cap, int* th, int* tw) const;
+    void layer_flops(int layer, uint64_t* f, uint64_t* d) const;
+    void output_device(const float** p, int* c, int* h, int* w) const;
+    int rows() const { return rows_; }
+    int cols() const { return cols_; }
+    int num_layers() const { return (int)net_.layers.size(); }
+    int kernel_count() const { return launches_; }
+
+  private:
+    struct LayerRT {
+        int halo_store = 0, halo_geom = 0;  // output packet halos (runtime)
+        PktDev pkt{};
+        DevArr<float> pkt_d;
+        DevArr<uint8_t> pkt_ext;
+        // state
+        BufDev acc{}, aux{};  // aux = trunc (truncation) or prev (maxpool)
+        DevArr<float> acc_d, aux_d;
+        float thr = 0.0f;
+        bool has_bias = false;
+        DevArr<float> bias_init;
+        // params
+        DevArr<float> w, wtc, scale;
+        int cin_pad = 0, cout_pad = 0;
+        DevArr<int> list;
+        int max_targets = 0;
+    };
+
+    void allocate(int th, int tw);
+    void build_packet(LayerRT& rt, int C, int t, int halo);
+    void enqueue(const float* frame_dev, int c, int h, int w, const float* h9, const float* roi_dev);
+    void finish_info(dfx_frame_info* info);
+    void ensure_staging(int c, int h, int w, bool host_frame);
+    PktDev in_packet(int idx) const { return idx == -1 ? in_pkt_ : lrt_[idx].pkt; }
+    Ctx ctx() const { return Ctx{d_frame_, d_slots_, rows_, cols_}; }
+
+    Net net_;
+    dfx_engine_config cfg_;
+    int device_ = 0;
+    cudaStream_t stream_ = nullptr;
+    int num_sms_ = 148;
+    bool initialized_ = false;
+    int64_t frame_index_ = 0;
+    int rows_ = 0, cols_ = 0;
+    Ledger ledger_;
+
+    std::vector<LayerRT> lrt_;
+    // input state
+    BufDev in_acc_{}, in_trunc_{};
+    DevArr<float> in_acc_d_, in_trunc_d_;
+    PktDev in_pkt_{};
+    DevArr<float> in_pkt_d_;
+    DevArr<uint8_t> in_pkt_ext_;
+    // input stage scratch
+    int canvas_pitch_ = 0;
+    DevArr<float> frame_d_, warped_d_, aligned_d_, roi_frame_d_, roi_warped_d_, roi_aligned_d_, roi_tmp_d_, fac_d_;
+    DevArr<uint8_t> fp_d_, valid_d_, roi_fp_d_, roi_valid_d_, sig_d_, sig2_d_, cov_d_, gate_d_;
+    // frame parameter block (device) + pinned staging
+    DevArr<uint8_t> params_d_;
+    uint8_t* params_hb_[2] = {nullptr, nullptr};
+    cudaEvent_t params_ev_[2] = {nullptr, nullptr};
+    int pslot_ = 0;
+    size_t params_bytes_ = 0, off_slots_ = 0, off_claims_ = 0, off_fresh_ = 0;
+    FrameDev* d_frame_ = nullptr;
+    SlotDev* d_slots_ = nullptr;
+    int* d_claims_ = nullptr;
+    uint8_t* d_fresh_ = nullptr;
+    int max_claims_ = 0;
+    // claims buffer table
+    DevArr<ClaimBuf> claim_bufs_;
+    int nclaim_bufs_ = 0;
+    // per-frame counters: [nl u64 flop_px][u64 dropped][nl int counts][nl * slots u32 tile_max]
+    DevArr<uint8_t> counters_d_;
+    size_t cnt_bytes_ = 0, off_dropped_ = 0, off_counts_ = 0, off_tmax_ = 0;
+    uint8_t* readback_h_ = nullptr;  // pinned: flop_px, dropped, input mask
+    // output
+    DevArr<float> out_d_;
+    // last frame
+    Placement place_{};
+    dfx_frame_info pending_{};
+    bool have_frame_ = false;
+    int launches_ = 0;
+};
+
+Engine::Engine(const dfx_net_desc* d, const dfx_engine_config* cfg, int device) : cfg_(*cfg), device_(device) {
+    net_ = validate_net(d, cfg->tile_size);
+    check(cfg_.tile_size >= 1, "engine: tile size must be >= 1");
+    check(cfg_.input_threshold >= 0.0f && cfg_.default_threshold >= 0.0f, "engine: thresholds must be >= 0");
+    check(cfg_.mask_dilation >= 0, "engine: mask dilation must be >= 0");
+    int ndev = 0;
+    CUDA_CHECK(cudaGetDeviceCount(&ndev));
+    check(ndev > 0, "no CUDA device (the B200 path has no CPU fallback)");
+    CUDA_CHECK(cudaSetDevice(device_));
+    CUDA_CHECK(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device_));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    lrt_.resize(net_.layers.size());
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    for (int i = 0; i < 2; ++i) {
+        if (params_hb_[i]) cudaFreeHost(params_hb_[i]);
+        if (params_ev_[i]) cudaEventDestroy(params_ev_[i]);
+    }
+    if (readback_h_) cudaFreeHost(readback_h_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::build_packet(LayerRT& rt, int C, int t, int halo) {
+    PktDev& p = rt.pkt;
+    p.C = C;
+    p.t = t;
+    p.halo = halo;
+    p.RT = (halo + t - 1) / t;
+    p.pitch_w = cols_ * t + 2 * halo;
+    p.ext_pitch = cols_ + 2 * p.RT;
+    rt.pkt_d.alloc((size_t)(rows_ * t + 2 * halo) * p.pitch_w * C);
+    rt.pkt_ext.alloc((size_t)(rows_ + 2 * p.RT) * p.ext_pitch);
+    CUDA_CHECK(cudaMemsetAsync(rt.pkt_ext.p, 0, rt.pkt_ext.n, stream_));
+    p.d = rt.pkt_d.p;
+    p.ext = rt.pkt_ext.p;
+}
+
+// engine.cpp:33-76: grid from the first placement, buffers per state.
+void Engine::allocate(int th, int tw) {
+    const int ring = cfg_.padded_convolutions ? net_.ring : 1;
+    rows_ = cfg_.grid_rows > 0 ? cfg_.grid_rows : th + 2 * ring;
+    cols_ = cfg_.grid_cols > 0 ? cfg_.grid_cols : tw + 2 * ring;
+    check(rows_ >= 1 && cols_ >= 1, "engine: bad grid dims");
+    check(rows_ * cfg_.tile_size + 64 < 32768 && cols_ * cfg_.tile_size + 64 < 32768, "engine: grid too large");
+    ledger_.init(rows_, cols_);
+    const int T = cfg_.tile_size, slots = rows_ * cols_;
+    const size_t tile_elems_in = (size_t)T * T * net_.in_channels;
+
+    in_acc_d_.alloc(slots * tile_elems_in);
+    in_trunc_d_.alloc(slots * tile_elems_in);
+    CUDA_CHECK(cudaMemsetAsync(in_acc_d_.p, 0, in_acc_d_.n * 4, stream_));
+    CUDA_CHECK(cudaMemsetAsync(in_trunc_d_.p, 0, in_trunc_d_.n * 4, stream_));
+    in_acc_ = {in_acc_d_.p, net_.in_channels, T};
+    in_trunc_ = {in_trunc_d_.p, net_.in_channels, T};
+    {
+        LayerRT tmp;
+        build_packet(tmp, net_.in_channels, T, 0);
+        in_pkt_ = tmp.pkt;
+        std::swap(in_pkt_d_.p, tmp.pkt_d.p);
+        std::swap(in_pkt_d_.n, tmp.pkt_d.n);
+        std::swap(in_pkt_ext_.p, tmp.pkt_ext.p);
+        std::swap(in_pkt_ext_.n, tmp.pkt_ext.n);
+    }
+    canvas_pitch_ = cols_ * T;
+    const size_t canvas_px = (size_t)rows_ * T * canvas_pitch_;
+    aligned_d_.alloc(canvas_px * net_.in_channels);
+    valid_d_.alloc(canvas_px);
+    sig_d_.alloc(canvas_px);
+    sig2_d_.alloc(canvas_px);
+    cov_d_.alloc(slots);
+    gate_d_.alloc(slots);
+    if (cfg_.roi_enabled) {
+        roi_aligned_d_.alloc(canvas_px);
+        roi_valid_d_.alloc(canvas_px);
+        roi_tmp_d_.alloc(canvas_px * 3);
+        fac_d_.alloc(canvas_px);
+    }
+
+    // layers (runtime halos follow the actual packets, engine.cpp:247-281)
+    std::vector<ClaimBuf> cbufs;
+    cbufs.push_back({in_acc_d_.p, nullptr, net_.in_channels, T});
+    cbufs.push_back({in_trunc_d_.p, nullptr, net_.in_channels, T});
+    for (int idx : net_.topo) {
+        const Layer& l = net_.layers[idx];
+        LayerRT& rt = lrt_[idx];
+        const int hin = l.in0 == -1 ? 0 : lrt_[l.in0].halo_store;
+        switch (l.kind) {
+            case DFX_CONV: {
+                rt.halo_geom = windowed_out_halo(hin, l.k, l.k / 2, l.stride);
+                rt.halo_store = cfg_.padded_convolutions ? rt.halo_geom : 0;
+                build_packet(rt, l.cout, l.tile, rt.halo_store);
+                rt.w.alloc(l.w.size());
+                CUDA_CHECK(cudaMemcpyAsync(rt.w.p, l.w.data(), l.w.size() * 4, cudaMemcpyHostToDevice, stream_));
+                rt.max_targets = (rows_ * l.tile + 2 * rt.halo_geom) * (cols_ * l.tile + 2 * rt.halo_geom);
+                rt.list.alloc(rt.max_targets);
+                if (cfg_.conv_mode == DFX_CONV_TF32X3) {
+                    rt.cin_pad = (l.cin + 7) / 8 * 8;
+                    rt.cout_pad = (l.cout + 15) / 16 * 16;
+                    std::vector<float> ws(conv_tc_weight_floats(rt.cin_pad, rt.cout_pad, l.k));
+                    conv_tc_prepare_weights(l.w.data(), l.cin, l.cout, l.k, rt.cin_pad, rt.cout_pad, ws.data());
+                    rt.wtc.alloc(ws.size());
+                    CUDA_CHECK(cudaMemcpy(rt.wtc.p, ws.data(), ws.size() * 4, cudaMemcpyHostToDevice));
+                }
+                break;
+            }
+            case DFX_RELU:
+            case DFX_TRUNCATE:
+            case DFX_OUTPUT: {
+                rt.halo_store = rt.halo_geom = 0;
+                build_packet(rt, l.in_channels, l.in_tile, 0);
+                float thr = 0.0f;
+                if (l.kind != DFX_OUTPUT && l.trunc_en)
+                    thr = (cfg_.override_net_thresholds || !l.has_thr) ? cfg_.default_threshold : l.thr;
+                rt.thr = thr;
+                const size_t n = (size_t)slots * l.in_tile * l.in_tile * l.in_channels;
+                rt.acc_d.alloc(n);
+                rt.aux_d.alloc(n);
+                CUDA_CHECK(cudaMemsetAsync(rt.acc_d.p, 0, n * 4, stream_));
+                CUDA_CHECK(cudaMemsetAsync(rt.aux_d.p, 0, n * 4, stream_));
+                rt.acc = {rt.acc_d.p, l.in_channels, l.in_tile};
+                rt.aux = {rt.aux_d.p, l.in_channels, l.in_tile};
+                std::vector<float> bias(l.in_channels, 0.0f);
+                if (l.in0 >= 0) bias = net_.layers[l.in0].beta;
+                rt.has_bias = std::any_of(bias.begin(), bias.end(), [](float b) { return b != 0.0f; });
+                cbufs.push_back({rt.acc_d.p, nullptr, l.in_channels, l.in_tile});
+                if (rt.has_bias) {
+                    rt.bias_init.alloc(bias.size());
+                    CUDA_CHECK(cudaMemcpy(rt.bias_init.p, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
+                    cbufs.push_back({rt.aux_d.p, rt.bias_init.p, l.in_channels, l.in_tile});
+                } else {
+                    cbufs.push_back({rt.aux_d.p, nullptr, l.in_channels, l.in_tile});
+                }
+                break;
+            }
+            case DFX_MAXPOOL: {
+                rt.halo_store = rt.halo_geom = windowed_out_halo(hin, l.pool_k, 0, l.pool_s);
+                build_packet(rt, l.in_channels, l.tile, rt.halo_store);
+                const size_t na = (size_t)slots * l.in_tile * l.in_tile * l.in_channels;
+                const size_t np = (size_t)slots * l.tile * l.tile * l.in_channels;
+                rt.acc_d.alloc(na);
+                rt.aux_d.alloc(np);
+                CUDA_CHECK(cudaMemsetAsync(rt.acc_d.p, 0, na * 4, stream_));
+                CUDA_CHECK(cudaMemsetAsync(rt.aux_d.p, 0, np * 4, stream_));
+                rt.acc = {rt.acc_d.p, l.in_channels, l.in_tile};
+                rt.aux = {rt.aux_d.p, l.in_channels, l.tile};
+                cbufs.push_back({rt.acc_d.p, nullptr, l.in_channels, l.in_tile});
+                cbufs.push_back({rt.aux_d.p, nullptr, l.in_channels, l.tile});
+                break;
+            }
+            case DFX_AVGPOOL:
+                rt.halo_store = rt.halo_geom = windowed_out_halo(hin, l.pool_k, 0, l.pool_s);
+                build_packet(rt, l.in_channels, l.tile, rt.halo_store);
+                break;
+            case DFX_UPSAMPLE:
+                rt.halo_store = rt.halo_geom = hin * l.factor;
+                build_packet(rt, l.in_channels, l.tile, rt.halo_store);
+                break;
+            case DFX_BATCHNORM:
+                rt.halo_store = rt.halo_geom = hin;
+                build_packet(rt, l.in_channels, l.tile, rt.halo_store);
+                rt.scale.alloc(l.bn_scale.size());
+                CUDA_CHECK(cudaMemcpy(rt.scale.p, l.bn_scale.data(), l.bn_scale.size() * 4, cudaMemcpyHostToDevice));
+                break;
+            case DFX_ADD: {
+                const int hb = l.in1 == -1 ? 0 : lrt_[l.in1].halo_store;
+                rt.halo_store = rt.halo_geom = std::max(hin, hb);
+                build_packet(rt, l.in_channels, l.tile, rt.halo_store);
+                break;
+            }
+        }
+    }
+    nclaim_bufs_ = (int)cbufs.size();
+    claim_bufs_.alloc(cbufs.size());
+    CUDA_CHECK(cudaMemcpy(claim_bufs_.p, cbufs.data(), cbufs.size() * sizeof(ClaimBuf), cudaMemcpyHostToDevice));
+
+    // frame parameter block
+    max_claims_ = slots;
+    off_slots_ = (sizeof(FrameDev) + 15) / 16 * 16;
+    off_claims_ = off_slots_ + (size_t)slots * sizeof(SlotDev);
+    off_fresh_ = off_claims_ + (size_t)max_claims_ * sizeof(int);
+    params_bytes_ = off_fresh_ + slots;
+    params_d_.alloc(params_bytes_);
+    for (int i = 0; i < 2; ++i) {
+        CUDA_CHECK(cudaMallocHost(&params_hb_[i], params_bytes_));
+        memset(params_hb_[i], 0, params_bytes_);
+        CUDA_CHECK(cudaEventCreateWithFlags(&params_ev_[i], cudaEventDisableTiming));
+    }
+    d_frame_ = reinterpret_cast<FrameDev*>(params_d_.p);
+    d_slots_ = reinterpret_cast<SlotDev*>(params_d_.p + off_slots_);
+    d_claims_ = reinterpret_cast<int*>(params_d_.p + off_claims_);
+    d_fresh_ = params_d_.p + off_fresh_;
+
+    const size_t nl = net_.layers.size();
+    off_dropped_ = nl * 8;
+    off_counts_ = off_dropped_ + 8;
+    off_tmax_ = (off_counts_ + nl * 4 + 15) / 16 * 16;
+    cnt_bytes_ = off_tmax_ + nl * (size_t)slots * 4;
+    counters_d_.alloc(cnt_bytes_);
+    CUDA_CHECK(cudaMallocHost(&readback_h_, nl * 8 + 8 + slots));
+
+    const int ot = net_.layers[net_.out_layer].in_tile;
+    out_d_.alloc((size_t)net_.layers[net_.out_layer].in_channels * rows_ * ot * cols_ * ot);
+    initialized_ = true;
+}
+
+void Engine::reset() {
+    // engine.cpp:93-108
+    if (!initialized_) return;
+    ledger_.clear();
+    CUDA_CHECK(cudaMemsetAsync(in_acc_d_.p, 0, in_acc_d_.n * 4, stream_));
+    CUDA_CHECK(cudaMemsetAsync(in_trunc_d_.p, 0, in_trunc_d_.n * 4, stream_));
+    for (auto& rt : lrt_) {
+        if (rt.acc_d.p) CUDA_CHECK(cudaMemsetAsync(rt.acc_d.p, 0, rt.acc_d.n * 4, stream_));
+        if (rt.aux_d.p) CUDA_CHECK(cudaMemsetAsync(rt.aux_d.p, 0, rt.aux_d.n * 4, stream_));
+    }
+}
+
+// engine.cpp:184-287 on device.
+void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h9, const float* roi_dev) {
+    check(c == net_.in_channels, "run_frame: input channel mismatch");
+    const int T = cfg_.tile_size;
+    // factor the integer translation out (engine.cpp:189-192)
+    const int64_t offx = (int64_t)std::llround(h9[2]), offy = (int64_t)std::llround(h9[5]);
+    const float tr[9] = {1, 0, (float)(-offx), 0, 1, (float)(-offy), 0, 0, 1};
+    float res[9], inv[9];
+    hom_compose(tr, h9, res);
+    hom_inverse(res, inv);  // warp() inverts first (alignment.cpp:59) and throws if singular
+    int64_t idx = 0, idy = 0;
+    const bool integer = hom_int_translation(res, &idx, &idy);
+    // snap_to_grid (alignment.cpp:106-166)
+    const int64_t ty0 = fdiv(offy, T), tx0 = fdiv(offx, T);
+    const int my = (int)(offy - ty0 * T), mx = (int)(offx - tx0 * T);
+    const int th0 = (int)cdiv(my + h, T), tw0 = (int)cdiv(mx + w, T);
+    const int max_r = initialized_ ? rows_ : cfg_.grid_rows, max_c = initialized_ ? cols_ : cfg_.grid_cols;
+    int drop_top = 0, drop_left = 0, th = th0, tw = tw0;
+    if (max_r > 0 && th0 > max_r) {
+        drop_top = (th0 - max_r) / 2;
+        th = max_r;
+    }
+    if (max_c > 0 && tw0 > max_c) {
+        drop_left = (tw0 - max_c) / 2;
+        tw = max_c;
+    }
+    const bool cropped = th != th0 || tw != tw0;
+    const int sy0 = drop_top * T - my, sx0 = drop_left * T - mx;
+    Placement pl;
+    pl.origin = {tx0 + drop_left, ty0 + drop_top};
+    pl.th = th;
+    pl.tw = tw;
+    if (!initialized_) allocate(th, tw);
+
+    dfx_frame_info& info = pending_;
+    memset(&info, 0, sizeof info);
+    info.frame_index = frame_index_;
+    info.origin_tx = pl.origin.tx;
+    info.origin_ty = pl.origin.ty;
+    info.tiles_h = th;
+    info.tiles_w = tw;
+    if (cropped && integer) {
+        // valid pixels of the shifted frame outside the crop window (alignment.cpp:233-242)
+        const int64_t fy = overlap(idy, idy + h, 0, h), fx = overlap(idx, idx + w, 0, w);
+        const int64_t ky = overlap(std::max<int64_t>(idy, 0), std::min<int64_t>(idy + h, h), sy0, sy0 + (int64_t)th * T);
+        const int64_t kx = overlap(std::max<int64_t>(idx, 0), std::min<int64_t>(idx + w, w), sx0, sx0 + (int64_t)tw * T);
+        info.dropped_pixels = fy * fx - ky * kx;
+    }
+
+    // plan (engine.cpp:206-214)
+    const int ring = cfg_.padded_convolutions ? net_.ring : 0;
+    check(th <= rows_ && tw <= cols_, "plan_frame: placement larger than grid");
+    Plan plan = ledger_.plan(pl, ring);
+    if (plan.full_reset) {
+        reset();
+        info.reset = 1;
+        plan = ledger_.plan(pl, ring);
+    }
+    ledger_.apply(plan, pl);
+    info.fresh = (int)plan.fresh.size();
+    info.evicted = plan.evicted;
+    check((int)plan.claims.size() <= max_claims_, "too many claims");
+
+    // parameter block
+    FrameDev F{};
+    F.otx = pl.origin.tx;
+    F.oty = pl.origin.ty;
+    F.th = th;
+    F.tw = tw;
+    F.base_sr = (int)floor_mod64(pl.origin.ty, rows_);
+    F.base_sc = (int)floor_mod64(pl.origin.tx, cols_);
+    F.nclaims = (int)plan.claims.size();
+    F.frame_h = h;
+    F.frame_w = w;
+    F.sy0 = sy0;
+    F.sx0 = sx0;
+    F.integer_path = integer ? 1 : 0;
+    F.idx = (int)idx;
+    F.idy = (int)idy;
+    F.roi = (cfg_.roi_enabled && roi_dev) ? 1 : 0;
+    for (int i = 0; i < 9; ++i) F.inv[i] = inv[i];
+    // the pinned block this frame writes may still feed an in-flight upload
+    pslot_ ^= 1;
+    uint8_t* params_h_ = params_hb_[pslot_];
+    CUDA_CHECK(cudaEventSynchronize(params_ev_[pslot_]));
+    memcpy(params_h_, &F, sizeof F);
+    SlotDev* hs = reinterpret_cast<SlotDev*>(params_h_ + off_slots_);
+    const auto& slots = ledger_.slots();
+    for (size_t i = 0; i < slots.size(); ++i)
+        hs[i] = SlotDev{slots[i].coord.tx, slots[i].coord.ty, slots[i].used ? 1 : 0, slots[i].covered ? 1 : 0};
+    int* hc = reinterpret_cast<int*>(params_h_ + off_claims_);
+    for (size_t i = 0; i < plan.claims.size(); ++i) hc[i] = ledger_.slot_index(plan.claims[i].coord);
+    uint8_t* hf = params_h_ + off_fresh_;
+    memset(hf, 0, (size_t)rows_ * cols_);
+    for (const Coord& t : plan.fresh) {
+        const int64_t r = t.ty - pl.origin.ty, cc = t.tx - pl.origin.tx;
+        if (r >= 0 && r < th && cc >= 0 && cc < tw) hf[r * tw + cc] = 1;
+    }
+    CUDA_CHECK(cudaMemcpyAsync(params_d_.p, params_h_, params_bytes_, cudaMemcpyHostToDevice, stream_));
+    CUDA_CHECK(cudaEventRecord(params_ev_[pslot_], stream_));
+    CUDA_CHECK(cudaMemsetAsync(counters_d_.p, 0, cnt_bytes_, stream_));
+    launches_ = 0;
+    const Ctx C = ctx();
+    cudaStream_t s = stream_;
+    auto* flop_px = reinterpret_cast<unsigned long long*>(counters_d_.p);
+    auto* dropped = reinterpret_cast<unsigned long long*>(counters_d_.p + off_dropped_);
+    int* counts = reinterpret_cast<int*>(counters_d_.p + off_counts_);
+    unsigned* tmax = reinterpret_cast<unsigned*>(counters_d_.p + off_tmax_);
+    const int nslots = rows_ * cols_;
+
+    // claims reset + implicit bias (buffer_manager.cpp:68-89)
+    launch_claims(C, s, d_claims_, claim_bufs_.p, nclaim_bufs_, max_claims_), ++launches_;
+
+    // input stage
+    if (!integer) launch_warp(C, s, frame_dev, c, warped_d_.p, fp_d_.p), ++launches_;
+    launch_align(C, s, frame_dev, warped_d_.p, fp_d_.p, c, aligned_d_.p, valid_d_.p, canvas_pitch_, T), ++launches_;
+    if (cropped && !integer) launch_count_dropped(C, s, fp_d_.p, T, dropped), ++launches_;
+    const float* fac = nullptr;
+    if (F.roi) {
+        if (!integer) launch_warp(C, s, roi_dev, 1, roi_warped_d_.p, roi_fp_d_.p), ++launches_;
+        launch_align(C, s, roi_dev, roi_warped_d_.p, roi_fp_d_.p, 1, roi_aligned_d_.p, roi_valid_d_.p, canvas_pitch_, T),
+            ++launches_;
+        launch_roi_factor(C, s, roi_aligned_d_.p, roi_tmp_d_.p, fac_d_.p, canvas_pitch_, T), launches_ += 2;
+        fac = fac_d_.p;
+    }
+    launch_coverage(C, s, valid_d_.p, canvas_pitch_, T, cov_d_.p), ++launches_;
+    launch_input_sig(C, s, aligned_d_.p, cov_d_.p, in_acc_, in_trunc_, fac, cfg_.input_threshold, canvas_pitch_, T,
+                     sig_d_.p), ++launches_;
+    const uint8_t* sig = sig_d_.p;
+    if (cfg_.noise_suppression) {
+        launch_noise(C, s, sig_d_.p, sig2_d_.p, canvas_pitch_, T), ++launches_;
+        sig = sig2_d_.p;
+    }
+    launch_gate(C, s, sig, cov_d_.p, d_fresh_, cfg_.mask_dilation, canvas_pitch_, T, gate_d_.p), ++launches_;
+    launch_input_apply(C, s, aligned_d_.p, cov_d_.p, gate_d_.p, in_acc_, in_trunc_, in_pkt_, canvas_pitch_), ++launches_;
+
+    // layers in topological order (engine.cpp:247-281)
+    for (int idx2 : net_.topo) {
+        const Layer& l = net_.layers[idx2];
+        LayerRT& rt = lrt_[idx2];
+        const PktDev a = in_packet(l.in0);
+        switch (l.kind) {
+            case DFX_CONV:
+                launch_conv_targets(C, s, a, l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom, rt.list.p, counts + idx2,
+                                    flop_px + idx2), ++launches_;
+                if (cfg_.conv_mode == DFX_CONV_EXACT)
+                    launch_conv_exact(C, s, a, rt.w.p, l.cin, l.cout, l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom,
+                                      rt.list.p, counts + idx2, rt.max_targets);
+                else
+                    launch_conv_tc(C, s, a, rt.wtc.p, l.cin, rt.cin_pad, l.cout, rt.cout_pad, l.k, l.stride, l.k / 2,
+                                   rt.pkt, rt.halo_geom, rt.list.p, counts + idx2, rt.max_targets, num_sms_);
+                ++launches_;
+                break;
+            case DFX_RELU:
+            case DFX_TRUNCATE:
+            case DFX_OUTPUT:
+                if (a.halo > 0) launch_ring_add(C, s, a, rt.aux), ++launches_;
+                launch_trunc_max(C, s, a, rt.aux, tmax + (size_t)idx2 * nslots), ++launches_;
+                launch_trunc_apply(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots, rt.thr,
+                                   l.kind == DFX_RELU ? 1 : 0, rt.pkt), ++launches_;
+                break;
+            case DFX_MAXPOOL:
+                launch_tile_add(C, s, a, rt.acc), ++launches_;
+                if (a.halo > 0) launch_ring_add(C, s, a, rt.acc), ++launches_;
+                launch_maxpool_out(C, s, a, rt.acc, rt.aux, l.pool_k, l.pool_s, rt.pkt, rt.halo_geom), ++launches_;
+                break;
+            case DFX_AVGPOOL: launch_avgpool(C, s, a, l.pool_k, l.pool_s, rt.pkt), ++launches_; break;
+            case DFX_UPSAMPLE: launch_upsample(C, s, a, l.factor, rt.pkt), ++launches_; break;
+            case DFX_BATCHNORM: launch_bn(C, s, a, rt.scale.p, rt.pkt), ++launches_; break;
+            case DFX_ADD: launch_add(C, s, a, in_packet(l.in1), rt.pkt), ++launches_; break;
+        }
+    }
+    const LayerRT& ort = lrt_[net_.out_layer];
+    launch_densify(C, s, ort.acc, ort.aux, out_d_.p), ++launches_;
+    CUDA_CHECK(cudaGetLastError());
+
+    // small readback: per-layer target counts, dropped, fired input tiles
+    const size_t nl = net_.layers.size();
+    CUDA_CHECK(cudaMemcpyAsync(readback_h_, counters_d_.p, nl * 8 + 8, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(readback_h_ + nl * 8 + 8, in_pkt_ext_.p, (size_t)rows_ * cols_, cudaMemcpyDeviceToHost, s));
+    place_ = pl;
+    const Layer& ol = net_.layers[net_.out_layer];
+    info.out_channels = ol.in_channels;
+    info.out_height = th * ol.in_tile;
+    info.out_width = tw * ol.in_tile;
+    ++frame_index_;
+    have_frame_ = true;
+}
+
+void Engine::finish_info(dfx_frame_info* out) {
+    dfx_frame_info info = pending_;
+    const size_t nl = net_.layers.size();
+    const uint64_t* fpx = reinterpret_cast<const uint64_t*>(readback_h_);
+    for (size_t i = 0; i < nl; ++i) {
+        const Layer& l = net_.layers[i];
+        if (l.kind != DFX_CONV) continue;
+        const uint64_t per_px = 2ull * l.k * l.k * l.cin * l.cout;
+        info.conv_flops += per_px * fpx[i];
+        info.dense_flops += per_px * (uint64_t)(place_.th * l.tile) * (uint64_t)(place_.tw * l.tile);
+    }
+    const uint64_t dropped = *reinterpret_cast<const uint64_t*>(readback_h_ + nl * 8);
+    if (dropped) info.dropped_pixels = (int64_t)dropped;
+    const uint8_t* mask = readback_h_ + nl * 8 + 8;
+    int cnt = 0;
+    for (int i = 0; i < place_.th * place_.tw; ++i) cnt += mask[(i / place_.tw) * in_pkt_.ext_pitch + i % place_.tw] ? 1 : 0;
+    info.update_rate = (double)cnt / ((double)place_.th * place_.tw);
+    pending_ = info;
+    if (out) *out = info;
+}
+
+void Engine::ensure_staging(int c, int h, int w, bool host_frame) {
+    const size_t fsz = (size_t)c * h * w, px = (size_t)h * w;
+    if (host_frame && frame_d_.n < fsz) frame_d_.alloc(fsz);
+    if (warped_d_.n < fsz) warped_d_.alloc(fsz);
+    if (fp_d_.n < px) fp_d_.alloc(px);
+    if (cfg_.roi_enabled && roi_frame_d_.n < px) {
+        roi_frame_d_.alloc(px);
+        roi_warped_d_.alloc(px);
+        roi_fp_d_.alloc(px);
+    }
+}
+
+void Engine::run_frame(const float* frame, int c, int h, int w, const float* h9, const float* roi,
+                       dfx_frame_info* info, float* out, size_t cap) {
+    check(c == net_.in_channels, "run_frame: input channel mismatch");
+    CUDA_CHECK(cudaSetDevice(device_));
+    const size_t fsz = (size_t)c * h * w;
+    ensure_staging(c, h, w, true);
+    CUDA_CHECK(cudaMemcpyAsync(frame_d_.p, frame, fsz * 4, cudaMemcpyHostToDevice, stream_));
+    const float* roi_dev = nullptr;
+    if (roi && cfg_.roi_enabled) {
+        CUDA_CHECK(cudaMemcpyAsync(roi_frame_d_.p, roi, (size_t)h * w * 4, cudaMemcpyHostToDevice, stream_));
+        roi_dev = roi_frame_d_.p;
+    }
+    enqueue(frame_d_.p, c, h, w, h9, roi_dev);
+    const size_t n = (size_t)pending_.out_channels * pending_.out_height * pending_.out_width;
+    if (out && cap >= n) {
+        // out_d_ is [C][th*t][tw*t] compact (k_densify writes the placement extent)
+        CUDA_CHECK(cudaMemcpyAsync(out, out_d_.p, n * 4, cudaMemcpyDeviceToHost, stream_));
+    }
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    CUDA_CHECK(cudaGetLastError());
+    finish_info(info);
+}
+
+void Engine::submit(const float* frame_dev, int c, int h, int w, const float* h9) {
+    CUDA_CHECK(cudaSetDevice(device_));
+    ensure_staging(c, h, w, false);
+    enqueue(frame_dev, c, h, w, h9, nullptr);
+}
+
+void Engine::sync(dfx_frame_info* info) {
+    CUDA_CHECK(cudaSetDevice(device_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    CUDA_CHECK(cudaGetLastError());
+    check(have_frame_, "no frame submitted");
+    finish_info(info);
+}
+
+void Engine::output_device(const float** p, int* c, int* h, int* w) const {
+    *p = out_d_.p;
+    *c = pending_.out_channels;
+    *h = pending_.out_height;
+    *w = pending_.out_width;
+}
+
+void Engine::input_mask(uint8_t* out, size_t cap, int* th, int* tw) const {
+    check(have_frame_, "no frame");
+    *th = place_.th;
+    *tw = place_.tw;
+    check(cap >= (size_t)place_.th * place_.tw, "mask buffer too small");
+    const size_t nl = net_.layers.size();
+    const uint8_t* mask = readback_h_ + nl * 8 + 8;
+    for (int r = 0; r < place_.th; ++r)
+        for (int c = 0; c < place_.tw; ++c) out[r * place_.tw + c] = mask[r * in_pkt_.ext_pitch + c] ? 1 : 0;
+}
+
+void Engine::layer_flops(int layer, uint64_t* f, uint64_t* d) const {
+    check(layer >= 0 && layer < (int)net_.layers.size(), "bad layer index");
+    const Layer& l = net_.layers[layer];
+    *f = *d = 0;
+    if (l.kind != DFX_CONV || !have_frame_) return;
+    const uint64_t per_px = 2ull * l.k * l.k * l.cin * l.cout;
+    *f = per_px * reinterpret_cast<const uint64_t*>(readback_h_)[layer];
+    *d = per_px * (uint64_t)(place_.th * l.tile) * (uint64_t)(place_.tw * l.tile);
+}
+
+void Engine::read_state(const std::string& layer, int which, float* out, size_t cap, int* c, int* h, int* w) {
+    check(initialized_, "no state buffer for layer " + layer);
+    BufDev b{};
+    if (layer == "input") {
+        if (which == DFX_STATE_ACC) b = in_acc_;
+        else if (which == DFX_STATE_TRUNC) b = in_trunc_;
+    } else {
+        const int i = net_.index_of(layer);
+        check(i >= 0, "no state buffer for layer " + layer);
+        const int k = net_.layers[i].kind;
+        const LayerRT& rt = lrt_[i];
+        if (k == DFX_RELU || k == DFX_TRUNCATE || k == DFX_OUTPUT) {
+            if (which == DFX_STATE_ACC) b = rt.acc;
+            else if (which == DFX_STATE_TRUNC) b = rt.aux;
+        } else if (k == DFX_MAXPOOL) {
+            if (which == DFX_STATE_ACC) b = rt.acc;
+            else if (which == DFX_STATE_PREV) b = rt.aux;
+        }
+    }
+    check(b.d != nullptr, "no state buffer for layer " + layer);
+    *c = b.C;
+    *h = rows_ * b.t;
+    *w = cols_ * b.t;
+    if (!out) return;
+    const size_t n = (size_t)b.C * rows_ * b.t * cols_ * b.t;
+    check(cap >= n, "state buffer too small");
+    std::vector<float> raw(n);
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    CUDA_CHECK(cudaMemcpy(raw.data(), b.d, n * 4, cudaMemcpyDeviceToHost));
+    const int t = b.t, C = b.C, PW = cols_ * t;
+    for (int sr = 0; sr < rows_; ++sr)
+        for (int sc = 0; sc < cols_; ++sc)
+            for (int y = 0; y < t; ++y)
+                for (int x = 0; x < t; ++x)
+                    for (int ch = 0; ch < C; ++ch)
+                        out[((size_t)ch * rows_ * t + sr * t + y) * PW + sc * t + x] =
+                            raw[((((size_t)sr * cols_ + sc) * t + y) * t + x) * C + ch];
+}
+
+void Engine::read_packet(const std::string& layer, float* out, size_t cap, int* c, int* gh, int* gw, int* halo,
+                         uint8_t* mask, size_t mask_cap) {
+    check(have_frame_, "no packet for layer " + layer);
+    PktDev p;
+    if (layer == "input") {
+        p = in_pkt_;
+    } else {
+        const int i = net_.index_of(layer);
+        check(i >= 0, "no packet for layer " + layer);
+        p = lrt_[i].pkt;
+    }
+    const int th = place_.th, tw = place_.tw;
+    *c = p.C;
+    *gh = th * p.t + 2 * p.halo;
+    *gw = tw * p.t + 2 * p.halo;
+    *halo = p.halo;
+    if (!out) return;
+    const size_t n = (size_t)p.C * *gh * *gw;
+    check(cap >= n && mask_cap >= (size_t)th * tw, "packet buffer too small");
+    const size_t rows_stored = (size_t)rows_ * p.t + 2 * p.halo;
+    std::vector<float> raw(rows_stored * p.pitch_w * p.C);
+    std::vector<uint8_t> ext((size_t)(rows_ + 2 * p.RT) * p.ext_pitch);
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    CUDA_CHECK(cudaMemcpy(raw.data(), p.d, raw.size() * 4, cudaMemcpyDeviceToHost));
+    CUDA_CHECK(cudaMemcpy(ext.data(), p.ext, ext.size(), cudaMemcpyDeviceToHost));
+    for (int y = -p.halo; y < th * p.t + p.halo; ++y)
+        for (int x = -p.halo; x < tw * p.t + p.halo; ++x) {
+            const int i = (int)floor_div64(y, p.t), j = (int)floor_div64(x, p.t);
+            const bool v = ext[(size_t)(i + p.RT) * p.ext_pitch + (j + p.RT)] != 0;
+            for (int ch = 0; ch < p.C; ++ch)
+                out[((size_t)ch * *gh + (y + p.halo)) * *gw + (x + p.halo)] =
+                    v ? raw[((size_t)(y + p.halo) * p.pitch_w + (x + p.halo)) * p.C + ch] : 0.0f;
+        }
+    for (int r = 0; r < th; ++r)
+        for (int cc = 0; cc < tw; ++cc) mask[r * tw + cc] = ext[(size_t)(r + p.RT) * p.ext_pitch + (cc + p.RT)] ? 1 : 0;
+}
+
+void Engine::read_ledger(int* used, int64_t* ty, int64_t* tx, uint8_t* covered, size_t cap) const {
+    check(initialized_, "engine not initialized");
+    const auto& s = ledger_.slots();
+    check(cap >= s.size(), "ledger buffer too small");
+    for (size_t i = 0; i < s.size(); ++i) {
+        used[i] = s[i].used;
+        ty[i] = s[i].coord.ty;
+        tx[i] = s[i].coord.tx;
+        covered[i] = s[i].covered;
+    }
+}
+
+}  // namespace dfx
+
+// ===================================================================== C-ABI
+using dfx::Engine;
+struct dfx_engine {
+    Engine* e;
+};
+
+namespace {
+thread_local std::string g_last;
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return DFX_OK;
+    } catch (const dfx::Error& e) {
+        g_last = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last = e.what();
+        return DFX_ERR;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+const char* dfx_last_error(void) { return g_last.c_str(); }
+
+void dfx_default_config(dfx_engine_config* c) {
+    // dflx::EngineConfig defaults (engine.hpp:10-21)
+    c->tile_size = 32;
+    c->grid_rows = 0;
+    c->grid_cols = 0;
+    c->input_threshold = 0.15f;
+    c->default_threshold = 0.02f;
+    c->override_net_thresholds = 0;
+    c->mask_dilation = 10;
+    c->roi_enabled = 0;
+    c->noise_suppression = 0;
+    c->padded_convolutions = 1;
+    c->conv_mode = DFX_CONV_TF32X3;
+}
+
+int dfx_engine_create(const dfx_net_desc* net, const dfx_engine_config* cfg, int device, dfx_engine** out) {
+    return guard([&] {
+        auto* h = new dfx_engine{nullptr};
+        try {
+            h->e = new Engine(net, cfg, device);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int dfx_engine_destroy(dfx_engine* e) {
+    return guard([&] {
+        if (!e) return;
+        delete e->e;
+        delete e;
+    });
+}
+
+int dfx_engine_run_frame(dfx_engine* e, const float* frame, int c, int h, int w, const float* h9, const float* roi,
+                         dfx_frame_info* info, float* out, size_t out_cap) {
+    return guard([&] { e->e->run_frame(frame, c, h, w, h9, roi, info, out, out_cap); });
+}
+int dfx_engine_submit_frame(dfx_engine* e, const float* frame_dev, int c, int h, int w, const float* h9) {
+    return guard([&] { e->e->submit(frame_dev, c, h, w, h9); });
+}
+int dfx_engine_sync(dfx_engine* e, dfx_frame_info* info) {
+    return guard([&] { e->e->sync(info); });
+}
+int dfx_engine_reset(dfx_engine* e) {
+    return guard([&] { e->e->reset(); });
+}
+int dfx_engine_output_device(dfx_engine* e, const float** p, int* c, int* h, int* w) {
+    return guard([&] { e->e->output_device(p, c, h, w); });
+}
+int dfx_engine_input_mask(dfx_engine* e, uint8_t* out, size_t cap, int* th, int* tw) {
+    return guard([&] { e->e->input_mask(out, cap, th, tw); });
+}
+int dfx_engine_num_layers(dfx_engine* e) { return e->e->num_layers(); }
+int dfx_engine_layer_flops(dfx_engine* e, int layer, uint64_t* f, uint64_t* d) {
+    return guard([&] { e->e->layer_flops(layer, f, d); });
+}
+int dfx_engine_grid(dfx_engine* e, int* rows, int* cols) {
+    return guard([&] {
+        *rows = e->e->rows();
+        *cols = e->e->cols();
+    });
+}
+int dfx_engine_read_state(dfx_engine* e, const char* layer, int which, float* out, size_t cap, int* c, int* h, int* w) {
+    return guard([&] { e->e->read_state(layer, which, out, cap, c, h, w); });
+}
+int dfx_engine_read_packet(dfx_engine* e, const char* layer, float* out, size_t cap, int* c, int* gh, int* gw, int* halo,
+                           uint8_t* mask, size_t mask_cap) {
+    return guard([&] { e->e->read_packet(layer, out, cap, c, gh, gw, halo, mask, mask_cap); });
+}
+int dfx_engine_read_ledger(dfx_engine* e, int* used, int64_t* ty, int64_t* tx, uint8_t* covered, size_t cap) {
+    return guard([&] { e->e->read_ledger(used, ty, tx, covered, cap); });
+}
+int dfx_engine_kernel_count(dfx_engine* e) { return e->e->kernel_count(); }
+
+void dfx_wrap_tile(int64_t tx, int64_t ty, int rows, int cols, int* row, int* col) {
+    // tile_grid.hpp:37-40
+    *row = (int)dfx::floor_mod64(ty, rows);
+    *col = (int)dfx::floor_mod64(tx, cols);
+}
+
+}  // extern "C"

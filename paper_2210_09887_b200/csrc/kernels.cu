@@ -1,0 +1,950 @@
+// B200 (sm_100a) kernels of the sparse frame-difference path: input stage,
+// claim reset / bias init, fused delta activation (truncation), sparse
+// pooling, linear packet ops, conv target compaction, exact-order CUDA-core
+// DeltaConv and the dense output. The tensor-core DeltaConv is conv_tc.cu.
+//
+// Bit-exactness: every arithmetic step that the reference performs in fp32 is
+// done here with explicitly rounded intrinsics (__fadd_rn / __fmul_rn /
+// __fdiv_rn, __dadd_rn / __dmul_rn) so nvcc cannot contract to FMA; the
+// reference's x86-64 build has no FMA (SURVEY §7 hard part 1).
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+
+namespace dfx {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ bool holds(const Ctx& c, const FrameDev& F, int qy, int qx) {
+    const SlotDev& s = c.slots[slot_of(F, c.rows, c.cols, qy, qx)];
+    return s.used && s.ty == F.oty + qy && s.tx == F.otx + qx;
+}
+
+// Base pointer of the slot tile holding placement-relative tile (qy, qx).
+__device__ __forceinline__ float* tile_ptr(const Ctx& c, const FrameDev& F, BufDev b, int qy, int qx) {
+    return b.d + (size_t)slot_of(F, c.rows, c.cols, qy, qx) * b.t * b.t * b.C;
+}
+
+// Value of a wrapped buffer at extent-relative pixel (y, x) of layer tile t.
+__device__ __forceinline__ float* buf_px(const Ctx& c, const FrameDev& F, BufDev b, int y, int x) {
+    const int qy = floor_div32(y, b.t), qx = floor_div32(x, b.t);
+    return tile_ptr(c, F, b, qy, qx) + ((size_t)(y - qy * b.t) * b.t + (x - qx * b.t)) * b.C;
+}
+
+// Packet sample with the reference's zero-fill semantics (delta_layers.hpp:37-41):
+// zero beyond the grown extent and in tiles the packet never wrote.
+__device__ __forceinline__ bool pkt_valid(const PktDev& p, int th, int tw, int y, int x) {
+    if (y < -p.halo || y >= th * p.t + p.halo || x < -p.halo || x >= tw * p.t + p.halo) return false;
+    const int i = floor_div32(y, p.t), j = floor_div32(x, p.t);
+    return p.ext[ext_idx(p, i, j)] != 0;
+}
+
+__device__ __forceinline__ float block_max(float v, float* red) {
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = l < (int)(blockDim.x >> 5) ? red[l] : 0.0f;
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (l == 0) red[0] = v;
+    }
+    __syncthreads();
+    return red[0];
+}
+
+int grid_for(long long n, int per_block = kThreads) {
+    long long g = (n + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    if (g > (1LL << 30)) g = 1LL << 30;
+    return (int)g;
+}
+
+// ----------------------------------------------------------------- warp
+// alignment.cpp:58-104, bilinear branch: inverse mapping in double, float weights.
+__global__ void k_warp(Ctx c, const float* __restrict__ frame, int C, float* __restrict__ warped,
+                       uint8_t* __restrict__ fp) {
+    const FrameDev& F = *c.f;
+    const int H = F.frame_h, W = F.frame_w;
+    const long long n = (long long)H * W;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / W), x = (int)(i % W);
+        const double xd = x, yd = y;
+        const double w = __dadd_rn(__dadd_rn(__dmul_rn((double)F.inv[6], xd), __dmul_rn((double)F.inv[7], yd)),
+                                   (double)F.inv[8]);
+        const double sx = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn((double)F.inv[0], xd), __dmul_rn((double)F.inv[1], yd)),
+                                              (double)F.inv[2]), w);
+        const double sy = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn((double)F.inv[3], xd), __dmul_rn((double)F.inv[4], yd)),
+                                              (double)F.inv[5]), w);
+        const bool ok = !(sx < 0.0 || sx > W - 1 || sy < 0.0 || sy > H - 1);
+        fp[i] = ok ? 1 : 0;
+        if (!ok) {
+            for (int ch = 0; ch < C; ++ch) warped[(size_t)ch * n + i] = 0.0f;
+            continue;
+        }
+        const int x0 = (int)floor(sx), y0 = (int)floor(sy);
+        const float fx = (float)(sx - x0), fy = (float)(sy - y0);
+        const int x1 = min(x0 + 1, W - 1), y1 = min(y0 + 1, H - 1);
+        const float gx = __fsub_rn(1.0f, fx), gy = __fsub_rn(1.0f, fy);
+        for (int ch = 0; ch < C; ++ch) {
+            const float* p = frame + (size_t)ch * n;
+            const float v00 = p[(size_t)y0 * W + x0], v01 = p[(size_t)y0 * W + x1];
+            const float v10 = p[(size_t)y1 * W + x0], v11 = p[(size_t)y1 * W + x1];
+            const float top = __fadd_rn(__fmul_rn(gx, v00), __fmul_rn(fx, v01));
+            const float bot = __fadd_rn(__fmul_rn(gx, v10), __fmul_rn(fx, v11));
+            warped[(size_t)ch * n + i] = __fadd_rn(__fmul_rn(gy, top), __fmul_rn(fy, bot));
+        }
+    }
+}
+
+// Canvas (aligned frame, alignment.cpp:106-166) in HWC with a valid map.
+// Warped pixel (cy + sy0, cx + sx0); integer path: warped = frame shifted by (idx, idy).
+__global__ void k_align(Ctx c, const float* __restrict__ frame, const float* __restrict__ warped,
+                        const uint8_t* __restrict__ fp, int C, float* __restrict__ aligned,
+                        uint8_t* __restrict__ valid, int pitch, int T) {
+    const FrameDev& F = *c.f;
+    const int ch_ = F.th * T, cw = F.tw * T;
+    const long long n = (long long)ch_ * cw;
+    const int H = F.frame_h, W = F.frame_w;
+    const size_t plane = (size_t)H * W;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int cy = (int)(i / cw), cx = (int)(i % cw);
+        const int y = cy + F.sy0, x = cx + F.sx0;
+        float* dst = aligned + ((size_t)cy * pitch + cx) * C;
+        bool ok = y >= 0 && y < H && x >= 0 && x < W;
+        if (ok && F.integer_path) {
+            const int sy = y - F.idy, sx = x - F.idx;
+            ok = sy >= 0 && sy < H && sx >= 0 && sx < W;
+            if (ok)
+                for (int ch = 0; ch < C; ++ch) dst[ch] = frame[(size_t)ch * plane + (size_t)sy * W + sx];
+        } else if (ok) {
+            ok = fp[(size_t)y * W + x] != 0;
+            for (int ch = 0; ch < C; ++ch) dst[ch] = warped[(size_t)ch * plane + (size_t)y * W + x];
+        }
+        if (!ok && !(!F.integer_path && y >= 0 && y < H && x >= 0 && x < W))
+            for (int ch = 0; ch < C; ++ch) dst[ch] = 0.0f;
+        valid[(size_t)cy * pitch + cx] = ok ? 1 : 0;
+    }
+}
+
+// Valid warped pixels that the crop dropped (alignment.cpp:131-164), bilinear path.
+__global__ void k_count_dropped(Ctx c, const uint8_t* __restrict__ fp, int T, unsigned long long* counter) {
+    const FrameDev& F = *c.f;
+    const int H = F.frame_h, W = F.frame_w;
+    const long long n = (long long)H * W;
+    unsigned long long local = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        if (!fp[i]) continue;
+        const int y = (int)(i / W), x = (int)(i % W);
+        const int cy = y - F.sy0, cx = x - F.sx0;
+        if (cy < 0 || cy >= F.th * T || cx < 0 || cx >= F.tw * T) ++local;
+    }
+    if (local) atomicAdd(counter, local);
+}
+
+// roi_factor_map (alignment.cpp:228-239) via window_max (:198-224), rows pass.
+__global__ void k_roi_rows(Ctx c, const float* __restrict__ roi, float* __restrict__ mid, int pitch, int T) {
+    const FrameDev& F = *c.f;
+    const int eh = F.th * T, ew = F.tw * T;
+    const long long n = (long long)eh * ew;
+    const size_t plane = (size_t)pitch * c.rows * T;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / ew), x = (int)(i % ew);
+        const int ks[3] = {10, 20, 40};
+        for (int q = 0; q < 3; ++q) {
+            const int lo = (ks[q] - 1) / 2, hi = ks[q] - 1 - lo;
+            float m = 0.0f;
+            for (int d = -lo; d <= hi; ++d) {
+                const int xx = x + d;
+                if (xx < 0 || xx >= ew) continue;
+                m = fmaxf(m, roi[(size_t)y * pitch + xx]);
+            }
+            mid[q * plane + (size_t)y * pitch + x] = m;
+        }
+    }
+}
+
+__global__ void k_roi_cols(Ctx c, const float* __restrict__ mid, float* __restrict__ fac, int pitch, int T) {
+    const FrameDev& F = *c.f;
+    const int eh = F.th * T, ew = F.tw * T;
+    const long long n = (long long)eh * ew;
+    const size_t plane = (size_t)pitch * c.rows * T;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / ew), x = (int)(i % ew);
+        const int ks[3] = {10, 20, 40};
+        float d[3];
+        for (int q = 0; q < 3; ++q) {
+            const int lo = (ks[q] - 1) / 2, hi = ks[q] - 1 - lo;
+            float m = 0.0f;
+            for (int dd = -lo; dd <= hi; ++dd) {
+                const int yy = y + dd;
+                if (yy < 0 || yy >= eh) continue;
+                m = fmaxf(m, mid[q * plane + (size_t)yy * pitch + x]);
+            }
+            d[q] = m;
+        }
+        const float mean = __fdiv_rn(__fadd_rn(__fadd_rn(d[0], d[1]), d[2]), 3.0f);
+        fac[(size_t)y * pitch + x] = __fadd_rn(0.4f, __fmul_rn(0.6f, mean));
+    }
+}
+
+// Tile covered iff any valid pixel (alignment.cpp:179-183).
+__global__ void k_coverage(Ctx c, const uint8_t* __restrict__ valid, int pitch, int T, uint8_t* __restrict__ cov) {
+    const FrameDev& F = *c.f;
+    const int ti = blockIdx.x;
+    if (ti >= F.th * F.tw) return;
+    const int tr = ti / F.tw, tc = ti % F.tw;
+    int any = 0;
+    for (int p = threadIdx.x; p < T * T && !any; p += blockDim.x) {
+        const int y = tr * T + p / T, x = tc * T + p % T;
+        if (valid[(size_t)y * pitch + x]) any = 1;
+    }
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) cov[ti] = any ? 1 : 0;
+}
+
+// Per-pixel significance of cand = trunc + raw (engine.cpp:119-139).
+__global__ void k_input_sig(Ctx c, const float* __restrict__ aligned, const uint8_t* __restrict__ cov, BufDev acc,
+                            BufDev trunc, const float* __restrict__ fac, float thr, int pitch, int T,
+                            uint8_t* __restrict__ sig) {
+    const FrameDev& F = *c.f;
+    const int eh = F.th * T, ew = F.tw * T;
+    const long long n = (long long)eh * ew;
+    const int C = acc.C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / ew), x = (int)(i % ew);
+        const int tr = y / T, tc = x / T;
+        const bool covered = cov[tr * F.tw + tc] != 0;
+        const size_t off = ((size_t)(y - tr * T) * T + (x - tc * T)) * C;
+        const float* a = tile_ptr(c, F, acc, tr, tc) + off;
+        const float* t = tile_ptr(c, F, trunc, tr, tc) + off;
+        const float* al = aligned + ((size_t)y * pitch + x) * C;
+        float m = 0.0f;
+        for (int ch = 0; ch < C; ++ch) {
+            const float raw = covered ? __fsub_rn(al[ch], a[ch]) : 0.0f;
+            m = fmaxf(m, fabsf(__fadd_rn(t[ch], raw)));
+        }
+        if (fac) m = __fmul_rn(m, fac[(size_t)y * pitch + x]);
+        sig[(size_t)y * pitch + x] = m > thr ? 1 : 0;
+    }
+}
+
+// Supporter rule: keep iff >= 2 significant in the clipped 3x3 (engine.cpp:142-158).
+__global__ void k_noise(Ctx c, const uint8_t* __restrict__ sig, uint8_t* __restrict__ out, int pitch, int T) {
+    const FrameDev& F = *c.f;
+    const int eh = F.th * T, ew = F.tw * T;
+    const long long n = (long long)eh * ew;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / ew), x = (int)(i % ew);
+        uint8_t keep = 0;
+        if (sig[(size_t)y * pitch + x]) {
+            int sup = 0;
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int yy = y + dy, xx = x + dx;
+                    if (yy < 0 || yy >= eh || xx < 0 || xx >= ew) continue;
+                    sup += sig[(size_t)yy * pitch + xx] ? 1 : 0;
+                }
+            keep = sup >= 2;
+        }
+        out[(size_t)y * pitch + x] = keep;
+    }
+}
+
+// Gate bit per tile (engine.cpp:160-180): covered and any significant pixel
+// within the (2r+1) max-filter reach of the tile (== tile OR of the dilated
+// map, window_max is a binary max filter), or fresh and covered.
+__global__ void k_gate(Ctx c, const uint8_t* __restrict__ sig, const uint8_t* __restrict__ cov,
+                       const uint8_t* __restrict__ fresh, int r, int pitch, int T, uint8_t* __restrict__ gate) {
+    const FrameDev& F = *c.f;
+    const int ti = blockIdx.x;
+    if (ti >= F.th * F.tw) return;
+    const int tr = ti / F.tw, tc = ti % F.tw;
+    const int eh = F.th * T, ew = F.tw * T;
+    if (!cov[ti]) {
+        if (threadIdx.x == 0) gate[ti] = 0;
+        return;
+    }
+    const int y0 = max(tr * T - r, 0), y1 = min((tr + 1) * T + r, eh);
+    const int x0 = max(tc * T - r, 0), x1 = min((tc + 1) * T + r, ew);
+    const int w = x1 - x0, n = (y1 - y0) * w;
+    int any = fresh[ti] != 0;
+    for (int p = threadIdx.x; p < n && !any; p += blockDim.x)
+        if (sig[(size_t)(y0 + p / w) * pitch + x0 + p % w]) any = 1;
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) gate[ti] = any ? 1 : 0;
+}
+
+// Number of row-chunks a tile of t rows is split into so one block moves
+// about kChunk floats (t rows of t*C floats each).
+constexpr int kChunk = 8192;
+__host__ __device__ inline int rows_per_chunk(int t, int C) {
+    const int r = kChunk / (t * C);
+    return r < 1 ? 1 : (r > t ? t : r);
+}
+__host__ __device__ inline int chunks_per_tile(int t, int C) {
+    const int r = rows_per_chunk(t, C);
+    return (t + r - 1) / r;
+}
+
+// Input truncation with the gate as fire (delta_layers.cpp:203-227 with
+// raw = aligned - acc, alignment.cpp:183-188): fire -> acc += trunc + raw,
+// trunc = 0, out = cand; else trunc += raw (the reference's double count).
+__global__ void k_input_apply(Ctx c, const float* __restrict__ aligned, const uint8_t* __restrict__ cov,
+                              const uint8_t* __restrict__ gate, BufDev acc, BufDev trunc, PktDev out, int pitch) {
+    const FrameDev& F = *c.f;
+    const int T = acc.t, C = acc.C;
+    const int nch = chunks_per_tile(T, C), rpc = rows_per_chunk(T, C);
+    const int ti = blockIdx.x / nch, ch = blockIdx.x % nch;
+    if (ti >= F.th * F.tw) return;
+    const int tr = ti / F.tw, tc = ti % F.tw;
+    const bool masked = cov[ti] && holds(c, F, tr, tc);
+    const bool fire = masked && gate[ti];
+    if (ch == 0 && threadIdx.x == 0) out.ext[ext_idx(out, tr, tc)] = fire ? 1 : 0;
+    if (!masked) return;
+    float* a = tile_ptr(c, F, acc, tr, tc);
+    float* t = tile_ptr(c, F, trunc, tr, tc);
+    const int row_len = T * C;
+    const int r0 = ch * rpc, r1 = min(T, r0 + rpc);
+    for (int e = threadIdx.x; e < (r1 - r0) * row_len; e += blockDim.x) {
+        const int yy = r0 + e / row_len, rem = e % row_len;
+        const size_t bi = (size_t)yy * row_len + rem;
+        const float al = aligned[((size_t)(tr * T + yy) * pitch + tc * T) * C + rem];
+        const float av = a[bi], tv = t[bi];
+        const float raw = __fsub_rn(al, av);
+        if (fire) {
+            const float cand = __fadd_rn(tv, raw);
+            a[bi] = __fadd_rn(av, cand);
+            t[bi] = 0.0f;
+            out.d[pkt_off(out, tr * T + yy, tc * T) + rem] = cand;
+        } else {
+            t[bi] = __fadd_rn(tv, raw);
+        }
+    }
+}
+
+// Claimed tiles of every buffer: zero, or the bias-init fill for truncated
+// buffers (buffer_manager.cpp:68-89, engine.cpp:78-91; fill after zero == fill).
+__global__ void k_claims(Ctx c, const int* __restrict__ claim_slots, const ClaimBuf* __restrict__ bufs) {
+    const FrameDev& F = *c.f;
+    const int ci = blockIdx.x;
+    if (ci >= F.nclaims) return;
+    const ClaimBuf b = bufs[blockIdx.y];
+    const size_t n = (size_t)b.t * b.t * b.C;
+    float* dst = b.d + (size_t)claim_slots[ci] * n;
+    if (!b.fill) {
+        float4* d4 = reinterpret_cast<float4*>(dst);
+        if ((n & 3) == 0) {
+            for (size_t i = threadIdx.x; i < n / 4; i += blockDim.x) d4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = 0.0f;
+        }
+    } else {
+        for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = b.fill[i % b.C];
+    }
+}
+
+// Ring ("dilated border") pixels of a packet added into a wrapped buffer at
+// owned slots (delta_layers.cpp:168-183 stash; :262-275 for maxpool acc).
+__global__ void k_ring_add(Ctx c, PktDev in, BufDev dst) {
+    const FrameDev& F = *c.f;
+    const int h = in.halo, t = in.t, C = in.C;
+    const int eh = F.th * t, ew = F.tw * t;
+    const int gw = ew + 2 * h;
+    // strips: top h x gw, bottom h x gw, left eh x h, right eh x h
+    const long long npx = 2LL * h * gw + 2LL * eh * h;
+    const long long n = npx * C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long p = i / C;
+        const int ch = (int)(i % C);
+        int y, x;
+        if (p < (long long)h * gw) {
+            y = -h + (int)(p / gw);
+            x = -h + (int)(p % gw);
+        } else if (p < 2LL * h * gw) {
+            const long long q = p - (long long)h * gw;
+            y = eh + (int)(q / gw);
+            x = -h + (int)(q % gw);
+        } else if (p < 2LL * h * gw + (long long)eh * h) {
+            const long long q = p - 2LL * h * gw;
+            y = (int)(q / h);
+            x = -h + (int)(q % h);
+        } else {
+            const long long q = p - 2LL * h * gw - (long long)eh * h;
+            y = (int)(q / h);
+            x = ew + (int)(q % h);
+        }
+        const int qy = floor_div32(y, t), qx = floor_div32(x, t);
+        if (!in.ext[ext_idx(in, qy, qx)]) continue;  // tile never written: zero
+        if (!holds(c, F, qy, qx)) continue;
+        float* b = buf_px(c, F, dst, y, x);
+        b[ch] = __fadd_rn(b[ch], in.d[pkt_off(in, y, x) + ch]);
+    }
+}
+
+// tile_max of |trunc + delta| over a masked owned tile (delta_layers.cpp:194-201).
+__global__ void k_trunc_max(Ctx c, PktDev in, BufDev trunc, unsigned* __restrict__ tile_max) {
+    __shared__ float red[32];
+    const FrameDev& F = *c.f;
+    const int T = in.t, C = in.C;
+    const int nch = chunks_per_tile(T, C), rpc = rows_per_chunk(T, C);
+    const int ti = blockIdx.x / nch, ch = blockIdx.x % nch;
+    if (ti >= F.th * F.tw) return;
+    const int tr = ti / F.tw, tc = ti % F.tw;
+    if (!in.ext[ext_idx(in, tr, tc)] || !holds(c, F, tr, tc)) return;
+    const float* tb = tile_ptr(c, F, trunc, tr, tc);
+    const int row_len = T * C;
+    const int r0 = ch * rpc, r1 = min(T, r0 + rpc);
+    float m = 0.0f;
+    if ((C & 3) == 0) {
+        const int rl4 = row_len / 4;
+        for (int e = threadIdx.x; e < (r1 - r0) * rl4; e += blockDim.x) {
+            const int yy = r0 + e / rl4, q = e % rl4;
+            const float4 tv = reinterpret_cast<const float4*>(tb + (size_t)yy * row_len)[q];
+            const float4 dv = reinterpret_cast<const float4*>(in.d + pkt_off(in, tr * T + yy, tc * T))[q];
+            m = fmaxf(m, fabsf(__fadd_rn(tv.x, dv.x)));
+            m = fmaxf(m, fabsf(__fadd_rn(tv.y, dv.y)));
+            m = fmaxf(m, fabsf(__fadd_rn(tv.z, dv.z)));
+            m = fmaxf(m, fabsf(__fadd_rn(tv.w, dv.w)));
+        }
+    } else {
+        for (int e = threadIdx.x; e < (r1 - r0) * row_len; e += blockDim.x) {
+            const int yy = r0 + e / row_len, rem = e % row_len;
+            m = fmaxf(m, fabsf(__fadd_rn(tb[(size_t)yy * row_len + rem], in.d[pkt_off(in, tr * T + yy, tc * T) + rem])));
+        }
+    }
+    m = block_max(m, red);
+    if (threadIdx.x == 0 && m > 0.0f) atomicMax(&tile_max[ti], __float_as_uint(m));
+}
+
+// Fire / fold per masked owned tile (delta_layers.cpp:203-228).
+__global__ void k_trunc_apply(Ctx c, PktDev in, BufDev acc, BufDev trunc, const unsigned* __restrict__ tile_max,
+                              float thr, int relu, PktDev out) {
+    const FrameDev& F = *c.f;
+    const int T = in.t, C = in.C;
+    const int nch = chunks_per_tile(T, C), rpc = rows_per_chunk(T, C);
+    const int ti = blockIdx.x / nch, ch = blockIdx.x % nch;
+    if (ti >= F.th * F.tw) return;
+    const int tr = ti / F.tw, tc = ti % F.tw;
+    const bool masked = in.ext[ext_idx(in, tr, tc)] && holds(c, F, tr, tc);
+    const float tmax = __uint_as_float(tile_max[ti]);
+    const bool fire = masked && tmax >= thr && tmax > 0.0f;
+    if (ch == 0 && threadIdx.x == 0) out.ext[ext_idx(out, tr, tc)] = fire ? 1 : 0;
+    if (!masked) return;
+    float* ab = tile_ptr(c, F, acc, tr, tc);
+    float* tb = tile_ptr(c, F, trunc, tr, tc);
+    const int row_len = T * C;
+    const int r0 = ch * rpc, r1 = min(T, r0 + rpc);
+    if ((C & 3) == 0) {
+        const int rl4 = row_len / 4;
+        for (int e = threadIdx.x; e < (r1 - r0) * rl4; e += blockDim.x) {
+            const int yy = r0 + e / rl4, q = e % rl4;
+            float4* t4 = reinterpret_cast<float4*>(tb + (size_t)yy * row_len) + q;
+            const float4 dv = reinterpret_cast<const float4*>(in.d + pkt_off(in, tr * T + yy, tc * T))[q];
+            float4 tv = *t4;
+            if (fire) {
+                float4* a4 = reinterpret_cast<float4*>(ab + (size_t)yy * row_len) + q;
+                const float4 pv = *a4;
+                float4 cd, nv, o;
+                cd.x = __fadd_rn(tv.x, dv.x); cd.y = __fadd_rn(tv.y, dv.y);
+                cd.z = __fadd_rn(tv.z, dv.z); cd.w = __fadd_rn(tv.w, dv.w);
+                nv.x = __fadd_rn(pv.x, cd.x); nv.y = __fadd_rn(pv.y, cd.y);
+                nv.z = __fadd_rn(pv.z, cd.z); nv.w = __fadd_rn(pv.w, cd.w);
+                if (relu) {
+                    o.x = __fsub_rn(fmaxf(nv.x, 0.f), fmaxf(pv.x, 0.f));
+                    o.y = __fsub_rn(fmaxf(nv.y, 0.f), fmaxf(pv.y, 0.f));
+                    o.z = __fsub_rn(fmaxf(nv.z, 0.f), fmaxf(pv.z, 0.f));
+                    o.w = __fsub_rn(fmaxf(nv.w, 0.f), fmaxf(pv.w, 0.f));
+                } else {
+                    o = cd;
+                }
+                *a4 = nv;
+                *t4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                reinterpret_cast<float4*>(out.d + pkt_off(out, tr * T + yy, tc * T))[q] = o;
+            } else {
+                tv.x = __fadd_rn(tv.x, dv.x); tv.y = __fadd_rn(tv.y, dv.y);
+                tv.z = __fadd_rn(tv.z, dv.z); tv.w = __fadd_rn(tv.w, dv.w);
+                *t4 = tv;
+            }
+        }
+    } else {
+        for (int e = threadIdx.x; e < (r1 - r0) * row_len; e += blockDim.x) {
+            const int yy = r0 + e / row_len, rem = e % row_len;
+            const size_t bi = (size_t)yy * row_len + rem;
+            const float dv = in.d[pkt_off(in, tr * T + yy, tc * T) + rem];
+            const float tv = tb[bi];
+            if (fire) {
+                const float cand = __fadd_rn(tv, dv), prev = ab[bi], nv = __fadd_rn(prev, cand);
+                ab[bi] = nv;
+                tb[bi] = 0.0f;
+                out.d[pkt_off(out, tr * T + yy, tc * T) + rem] =
+                    relu ? __fsub_rn(fmaxf(nv, 0.f), fmaxf(prev, 0.f)) : cand;
+            } else {
+                tb[bi] = __fadd_rn(tv, dv);
+            }
+        }
+    }
+}
+
+// acc += delta on masked owned tiles (delta_layers.cpp:253-261).
+__global__ void k_tile_add(Ctx c, PktDev in, BufDev acc) {
+    const FrameDev& F = *c.f;
+    const int T = in.t, C = in.C;
+    const int nch = chunks_per_tile(T, C), rpc = rows_per_chunk(T, C);
+    const int ti = blockIdx.x / nch, ch = blockIdx.x % nch;
+    if (ti >= F.th * F.tw) return;
+    const int tr = ti / F.tw, tc = ti % F.tw;
+    if (!in.ext[ext_idx(in, tr, tc)] || !holds(c, F, tr, tc)) return;
+    float* ab = tile_ptr(c, F, acc, tr, tc);
+    const int row_len = T * C;
+    const int r0 = ch * rpc, r1 = min(T, r0 + rpc);
+    for (int e = threadIdx.x; e < (r1 - r0) * row_len; e += blockDim.x) {
+        const int yy = r0 + e / row_len, rem = e % row_len;
+        const size_t bi = (size_t)yy * row_len + rem;
+        ab[bi] = __fadd_rn(ab[bi], in.d[pkt_off(in, tr * T + yy, tc * T) + rem]);
+    }
+}
+
+// Target test of a windowed op (delta_layers.cpp:34-70): output (oy, ox)
+// whose window [o*s - back, o*s - back + span) meets a masked input tile
+// grown by the input halo.
+__device__ __forceinline__ bool is_target(const PktDev& in, int th, int tw, int oy, int ox, int span, int back,
+                                          int s) {
+    const int iy0 = oy * s - back - in.halo, iy1 = oy * s - back + span - 1 + in.halo;
+    const int ix0 = ox * s - back - in.halo, ix1 = ox * s - back + span - 1 + in.halo;
+    const int tr0 = max(floor_div32(iy0, in.t), 0), tr1 = min(floor_div32(iy1, in.t), th - 1);
+    const int tc0 = max(floor_div32(ix0, in.t), 0), tc1 = min(floor_div32(ix1, in.t), tw - 1);
+    for (int tr = tr0; tr <= tr1; ++tr)
+        for (int tc = tc0; tc <= tc1; ++tc)
+            if (in.ext[ext_idx(in, tr, tc)]) return true;
+    return false;
+}
+
+// Block index -> extended output tile (i, j) in [-RT, th+RT) x [-RT, tw+RT).
+__device__ __forceinline__ bool ext_tile(const FrameDev& F, const PktDev& out, int& i, int& j) {
+    const int ew = F.tw + 2 * out.RT;
+    const int b = blockIdx.x;
+    if (b >= (F.th + 2 * out.RT) * ew) return false;
+    i = b / ew - out.RT;
+    j = b % ew - out.RT;
+    return true;
+}
+
+// Pixel range of ext tile (i, j) clipped to the stored grown extent.
+__device__ __forceinline__ void tile_px_range(const FrameDev& F, const PktDev& out, int i, int j, int& y0, int& y1,
+                                              int& x0, int& x1) {
+    const int t = out.t, h = out.halo;
+    y0 = max(i * t, -h);
+    y1 = min((i + 1) * t, F.th * t + h);
+    x0 = max(j * t, -h);
+    x1 = min((j + 1) * t, F.tw * t + h);
+}
+
+// Conv target compaction + output ext map + zero fill of non-targets.
+// Iterates the GEOMETRIC grown extent (out_halo_geom) so FLOPs count ring
+// targets even when the stored packet is cropped (padded_convolutions=false,
+// engine.cpp:254-264).
+__global__ void k_conv_targets(Ctx c, PktDev in, int k, int s, int r, PktDev out, int hg, int* __restrict__ list,
+                               int* __restrict__ count, unsigned long long* __restrict__ flop_px) {
+    __shared__ int s_cnt, s_base;
+    const FrameDev& F = *c.f;
+    const int RTg = (hg + out.t - 1) / out.t;
+    const int ew = F.tw + 2 * RTg;
+    const int b = blockIdx.x;
+    if (b >= (F.th + 2 * RTg) * ew) return;
+    const int i = b / ew - RTg, j = b % ew - RTg;
+    const int t = out.t;
+    // geometric range
+    const int gy0 = max(i * t, -hg), gy1 = min((i + 1) * t, F.th * t + hg);
+    const int gx0 = max(j * t, -hg), gx1 = min((j + 1) * t, F.tw * t + hg);
+    const bool stored_tile = i >= -out.RT && i < F.th + out.RT && j >= -out.RT && j < F.tw + out.RT;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const int w = gx1 - gx0, n = (gy1 - gy0) * w;
+    int geo_targets = 0, any_stored = 0;
+    for (int p = threadIdx.x; p < n; p += blockDim.x) {
+        const int oy = gy0 + p / w, ox = gx0 + p % w;
+        if (is_target(in, F.th, F.tw, oy, ox, k, r, s)) {
+            ++geo_targets;
+            if (oy >= -out.halo && oy < F.th * t + out.halo && ox >= -out.halo && ox < F.tw * t + out.halo)
+                any_stored = 1;
+        }
+    }
+    any_stored = __syncthreads_or(any_stored);
+    if (geo_targets) atomicAdd(flop_px, (unsigned long long)geo_targets);
+    if (stored_tile && threadIdx.x == 0) out.ext[ext_idx(out, i, j)] = any_stored ? 1 : 0;
+    if (!stored_tile || !any_stored) return;
+    int y0, y1, x0, x1;
+    tile_px_range(F, out, i, j, y0, y1, x0, x1);
+    const int sw = x1 - x0, sn = (y1 - y0) * sw;
+    // pass 1: count + zero non-targets
+    for (int p = threadIdx.x; p < sn; p += blockDim.x) {
+        const int oy = y0 + p / sw, ox = x0 + p % sw;
+        if (is_target(in, F.th, F.tw, oy, ox, k, r, s)) {
+            atomicAdd(&s_cnt, 1);
+        } else {
+            float* d = out.d + pkt_off(out, oy, ox);
+            for (int ch = 0; ch < out.C; ++ch) d[ch] = 0.0f;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = atomicAdd(count, s_cnt), s_cnt = 0;
+    __syncthreads();
+    for (int p = threadIdx.x; p < sn; p += blockDim.x) {
+        const int oy = y0 + p / sw, ox = x0 + p % sw;
+        if (is_target(in, F.th, F.tw, oy, ox, k, r, s)) {
+            const int slot = s_base + atomicAdd(&s_cnt, 1);
+            list[slot] = ((oy + hg) << 16) | (ox + hg);
+        }
+    }
+}
+
+// Exact-order DeltaConv on CUDA cores: acc += sample * w in the reference's
+// i -> ky -> kx order with separate fp32 rounding (delta_layers.cpp:121-134),
+// hence bit-identical outputs. Work item = 32 target pixels x 64 couts.
+constexpr int kXP = 32, kXO = 64;
+__global__ void __launch_bounds__(256) k_conv_exact(Ctx c, PktDev in, const float* __restrict__ w, int cin, int cout,
+                                                    int k, int s, int r, PktDev out, int hg, const int* __restrict__ list,
+                                                    const int* __restrict__ count, int ci_chunk) {
+    extern __shared__ float smem[];
+    __shared__ int s_y[kXP], s_x[kXP];
+    const FrameDev& F = *c.f;
+    const int K2 = k * k;
+    float* s_in = smem;                          // [ci_chunk][K2][kXP]
+    float* s_w = smem + ci_chunk * K2 * kXP;     // [kXO][ci_chunk*K2]
+    const int n = *count;
+    const int nob = (cout + kXO - 1) / kXO;
+    const int items = ((n + kXP - 1) / kXP) * nob;
+    const int p = threadIdx.x % kXP, og = threadIdx.x / kXP;  // og in [0, 8)
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int chunk = item / nob, o0 = (item % nob) * kXO;
+        __syncthreads();
+        if (threadIdx.x < kXP) {
+            const int idx = chunk * kXP + threadIdx.x;
+            if (idx < n) {
+                const int v = list[idx];
+                s_y[threadIdx.x] = (v >> 16) - hg;
+                s_x[threadIdx.x] = (v & 0xffff) - hg;
+            } else {
+                s_y[threadIdx.x] = INT_MIN / 4;
+                s_x[threadIdx.x] = INT_MIN / 4;
+            }
+        }
+        float acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+        for (int i0 = 0; i0 < cin; i0 += ci_chunk) {
+            const int ci = min(ci_chunk, cin - i0);
+            __syncthreads();
+            for (int e = threadIdx.x; e < ci * K2 * kXP; e += blockDim.x) {
+                const int pp = e % kXP, kk = (e / kXP) % K2, ii = e / (kXP * K2);
+                const int iy = s_y[pp] * s - r + kk / k, ix = s_x[pp] * s - r + kk % k;
+                float v = 0.0f;
+                if (s_y[pp] > INT_MIN / 8 && pkt_valid(in, F.th, F.tw, iy, ix)) v = in.d[pkt_off(in, iy, ix) + i0 + ii];
+                s_in[(ii * K2 + kk) * kXP + pp] = v;
+            }
+            for (int e = threadIdx.x; e < kXO * ci * K2; e += blockDim.x) {
+                const int oo = e / (ci * K2), rem = e % (ci * K2);
+                const int o = o0 + oo;
+                s_w[oo * (ci_chunk * K2) + rem] = o < cout ? w[((size_t)o * cin + i0) * K2 + rem] : 0.0f;
+            }
+            __syncthreads();
+            for (int ii = 0; ii < ci; ++ii)
+                for (int kk = 0; kk < K2; ++kk) {
+                    const float a = s_in[(ii * K2 + kk) * kXP + p];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        acc[q] = __fadd_rn(acc[q], __fmul_rn(a, s_w[(og + 8 * q) * (ci_chunk * K2) + ii * K2 + kk]));
+                }
+        }
+        const int idx = chunk * kXP + p;
+        if (idx < n) {
+            float* d = out.d + pkt_off(out, s_y[p], s_x[p]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int o = o0 + og + 8 * q;
+                if (o < cout) d[o] = acc[q];
+            }
+        }
+    }
+}
+
+// Max pool output (delta_layers.cpp:277-317): m over the k x k window of the
+// accumulated input (first-element init, non-owned tiles read 0), out = m - prev,
+// prev = m, on owned target outputs.
+__global__ void k_maxpool_out(Ctx c, PktDev in, BufDev acc, BufDev prev, int k, int s, PktDev out, int hg) {
+    const FrameDev& F = *c.f;
+    int i, j;
+    if (!ext_tile(F, out, i, j)) return;
+    int y0, y1, x0, x1;
+    tile_px_range(F, out, i, j, y0, y1, x0, x1);
+    const int w = x1 - x0, n = (y1 - y0) * w;
+    int any = 0;
+    for (int p = threadIdx.x; p < n && !any; p += blockDim.x)
+        if (is_target(in, F.th, F.tw, y0 + p / w, x0 + p % w, k, 0, s)) any = 1;
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) out.ext[ext_idx(out, i, j)] = any ? 1 : 0;
+    if (!any) return;
+    const int C = out.C;
+    const bool out_owned = holds(c, F, i, j);
+    for (long long e = threadIdx.x; e < (long long)n * C; e += blockDim.x) {
+        const int pp = (int)(e / C), ch = (int)(e % C);
+        const int oy = y0 + pp / w, ox = x0 + pp % w;
+        float* d = out.d + pkt_off(out, oy, ox) + ch;
+        if (!out_owned || !is_target(in, F.th, F.tw, oy, ox, k, 0, s)) {
+            *d = 0.0f;
+            continue;
+        }
+        float m = 0.0f;
+        bool first = true;
+        for (int ky = 0; ky < k; ++ky)
+            for (int kx = 0; kx < k; ++kx) {
+                const int iy = oy * s + ky, ix = ox * s + kx;
+                const int qy = floor_div32(iy, in.t), qx = floor_div32(ix, in.t);
+                const float v = holds(c, F, qy, qx) ? buf_px(c, F, acc, iy, ix)[ch] : 0.0f;
+                m = first ? v : fmaxf(m, v);
+                first = false;
+            }
+        float* pv = buf_px(c, F, prev, oy, ox) + ch;
+        *d = __fsub_rn(m, *pv);
+        *pv = m;
+    }
+}
+
+// Average pool (delta_layers.cpp:320-349): sum in (ky, kx) order times 1/k^2.
+__global__ void k_avgpool(Ctx c, PktDev in, int k, int s, PktDev out) {
+    const FrameDev& F = *c.f;
+    int i, j;
+    if (!ext_tile(F, out, i, j)) return;
+    int y0, y1, x0, x1;
+    tile_px_range(F, out, i, j, y0, y1, x0, x1);
+    const int w = x1 - x0, n = (y1 - y0) * w;
+    int any = 0;
+    for (int p = threadIdx.x; p < n && !any; p += blockDim.x)
+        if (is_target(in, F.th, F.tw, y0 + p / w, x0 + p % w, k, 0, s)) any = 1;
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) out.ext[ext_idx(out, i, j)] = any ? 1 : 0;
+    if (!any) return;
+    const int C = out.C;
+    const float inv = __fdiv_rn(1.0f, (float)(k * k));
+    for (long long e = threadIdx.x; e < (long long)n * C; e += blockDim.x) {
+        const int pp = (int)(e / C), ch = (int)(e % C);
+        const int oy = y0 + pp / w, ox = x0 + pp % w;
+        float v = 0.0f;
+        if (is_target(in, F.th, F.tw, oy, ox, k, 0, s)) {
+            float sum = 0.0f;
+            for (int ky = 0; ky < k; ++ky)
+                for (int kx = 0; kx < k; ++kx) {
+                    const int iy = oy * s + ky, ix = ox * s + kx;
+                    if (pkt_valid(in, F.th, F.tw, iy, ix)) sum = __fadd_rn(sum, in.d[pkt_off(in, iy, ix) + ch]);
+                    else sum = __fadd_rn(sum, 0.0f);
+                }
+            v = __fmul_rn(sum, inv);
+        }
+        out.d[pkt_off(out, oy, ox) + ch] = v;
+    }
+}
+
+// Nearest upsample (delta_layers.cpp:351-363).
+__global__ void k_upsample(Ctx c, PktDev in, int f, PktDev out) {
+    const FrameDev& F = *c.f;
+    int i, j;
+    if (!ext_tile(F, out, i, j)) return;
+    const bool v = in.ext[ext_idx(in, i, j)] != 0;
+    if (threadIdx.x == 0) out.ext[ext_idx(out, i, j)] = v ? 1 : 0;
+    if (!v) return;
+    int y0, y1, x0, x1;
+    tile_px_range(F, out, i, j, y0, y1, x0, x1);
+    const int w = x1 - x0, n = (y1 - y0) * w, C = out.C;
+    for (long long e = threadIdx.x; e < (long long)n * C; e += blockDim.x) {
+        const int pp = (int)(e / C), ch = (int)(e % C);
+        const int oy = y0 + pp / w, ox = x0 + pp % w;
+        out.d[pkt_off(out, oy, ox) + ch] = in.d[pkt_off(in, floor_div32(oy, f), floor_div32(ox, f)) + ch];
+    }
+}
+
+// BatchNorm scale (delta_layers.cpp:365-376).
+__global__ void k_bn(Ctx c, PktDev in, const float* __restrict__ scale, PktDev out) {
+    const FrameDev& F = *c.f;
+    int i, j;
+    if (!ext_tile(F, out, i, j)) return;
+    const bool v = in.ext[ext_idx(in, i, j)] != 0;
+    if (threadIdx.x == 0) out.ext[ext_idx(out, i, j)] = v ? 1 : 0;
+    if (!v) return;
+    int y0, y1, x0, x1;
+    tile_px_range(F, out, i, j, y0, y1, x0, x1);
+    const int w = x1 - x0, n = (y1 - y0) * w, C = out.C;
+    for (long long e = threadIdx.x; e < (long long)n * C; e += blockDim.x) {
+        const int pp = (int)(e / C), ch = (int)(e % C);
+        const int oy = y0 + pp / w, ox = x0 + pp % w;
+        out.d[pkt_off(out, oy, ox) + ch] = __fmul_rn(in.d[pkt_off(in, oy, ox) + ch], scale[ch]);
+    }
+}
+
+__device__ __forceinline__ bool ext_in_range(const FrameDev& F, const PktDev& p, int i, int j) {
+    return i >= -p.RT && i < F.th + p.RT && j >= -p.RT && j < F.tw + p.RT;
+}
+
+// Add: zero-extended sum, mask OR (delta_layers.cpp:378-393).
+__global__ void k_add(Ctx c, PktDev a, PktDev b, PktDev out) {
+    const FrameDev& F = *c.f;
+    int i, j;
+    if (!ext_tile(F, out, i, j)) return;
+    const bool va = ext_in_range(F, a, i, j) && a.ext[ext_idx(a, i, j)];
+    const bool vb = ext_in_range(F, b, i, j) && b.ext[ext_idx(b, i, j)];
+    if (threadIdx.x == 0) out.ext[ext_idx(out, i, j)] = (va || vb) ? 1 : 0;
+    if (!va && !vb) return;
+    int y0, y1, x0, x1;
+    tile_px_range(F, out, i, j, y0, y1, x0, x1);
+    const int w = x1 - x0, n = (y1 - y0) * w, C = out.C;
+    for (long long e = threadIdx.x; e < (long long)n * C; e += blockDim.x) {
+        const int pp = (int)(e / C), ch = (int)(e % C);
+        const int oy = y0 + pp / w, ox = x0 + pp % w;
+        const float sa = (va && pkt_valid(a, F.th, F.tw, oy, ox)) ? a.d[pkt_off(a, oy, ox) + ch] : 0.0f;
+        const float sb = (vb && pkt_valid(b, F.th, F.tw, oy, ox)) ? b.d[pkt_off(b, oy, ox) + ch] : 0.0f;
+        out.d[pkt_off(out, oy, ox) + ch] = __fadd_rn(sa, sb);
+    }
+}
+
+// Output = acc + trunc over the placement, CHW (delta_layers.cpp:395-400).
+__global__ void k_densify(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ out) {
+    const FrameDev& F = *c.f;
+    const int t = acc.t, C = acc.C;
+    const int oh = F.th * t, ow = F.tw * t;
+    const long long n = (long long)C * oh * ow;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % ow);
+        const int y = (int)((i / ow) % oh);
+        const int ch = (int)(i / ((long long)ow * oh));
+        const int qy = y / t, qx = x / t;
+        const size_t off = (size_t)slot_of(F, c.rows, c.cols, qy, qx) * t * t * C +
+                           ((size_t)(y - qy * t) * t + (x - qx * t)) * C + ch;
+        out[i] = __fadd_rn(acc.d[off], trunc.d[off]);
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- launchers
+static int num_sms_cached() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+static int persistent_grid(long long work) {
+    const long long cap = (long long)num_sms_cached() * 8;
+    long long g = (work + kThreads - 1) / kThreads;
+    if (g > cap) g = cap;
+    return g < 1 ? 1 : (int)g;
+}
+
+void launch_warp(const Ctx& c, cudaStream_t s, const float* frame, int C, float* warped, uint8_t* fp) {
+    // frame dims are per-frame but bounded by the staging buffer; use a persistent grid
+    k_warp<<<num_sms_cached() * 8, kThreads, 0, s>>>(c, frame, C, warped, fp);
+}
+void launch_align(const Ctx& c, cudaStream_t s, const float* frame, const float* warped, const uint8_t* fp, int C,
+                  float* aligned, uint8_t* valid, int pitch, int T) {
+    k_align<<<persistent_grid((long long)c.rows * T * pitch), kThreads, 0, s>>>(c, frame, warped, fp, C, aligned,
+                                                                               valid, pitch, T);
+}
+void launch_count_dropped(const Ctx& c, cudaStream_t s, const uint8_t* fp, int T, unsigned long long* counter) {
+    k_count_dropped<<<num_sms_cached() * 4, kThreads, 0, s>>>(c, fp, T, counter);
+}
+void launch_roi_factor(const Ctx& c, cudaStream_t s, const float* roi, float* tmp3, float* fac, int pitch, int T) {
+    const long long n = (long long)c.rows * T * pitch;
+    k_roi_rows<<<persistent_grid(n), kThreads, 0, s>>>(c, roi, tmp3, pitch, T);
+    k_roi_cols<<<persistent_grid(n), kThreads, 0, s>>>(c, tmp3, fac, pitch, T);
+}
+void launch_coverage(const Ctx& c, cudaStream_t s, const uint8_t* valid, int pitch, int T, uint8_t* cov) {
+    k_coverage<<<c.rows * c.cols, kThreads, 0, s>>>(c, valid, pitch, T, cov);
+}
+void launch_input_sig(const Ctx& c, cudaStream_t s, const float* aligned, const uint8_t* cov, BufDev acc,
+                      BufDev trunc, const float* fac, float thr, int pitch, int T, uint8_t* sig) {
+    k_input_sig<<<persistent_grid((long long)c.rows * T * pitch), kThreads, 0, s>>>(c, aligned, cov, acc, trunc, fac,
+                                                                                   thr, pitch, T, sig);
+}
+void launch_noise(const Ctx& c, cudaStream_t s, const uint8_t* sig, uint8_t* out, int pitch, int T) {
+    k_noise<<<persistent_grid((long long)c.rows * T * pitch), kThreads, 0, s>>>(c, sig, out, pitch, T);
+}
+void launch_gate(const Ctx& c, cudaStream_t s, const uint8_t* sig, const uint8_t* cov, const uint8_t* fresh,
+                 int dilation, int pitch, int T, uint8_t* gate) {
+    k_gate<<<c.rows * c.cols, kThreads, 0, s>>>(c, sig, cov, fresh, dilation, pitch, T, gate);
+}
+void launch_input_apply(const Ctx& c, cudaStream_t s, const float* aligned, const uint8_t* cov, const uint8_t* gate,
+                        BufDev acc, BufDev trunc, PktDev out, int pitch) {
+    const int nch = chunks_per_tile(acc.t, acc.C);
+    k_input_apply<<<c.rows * c.cols * nch, kThreads, 0, s>>>(c, aligned, cov, gate, acc, trunc, out, pitch);
+}
+void launch_claims(const Ctx& c, cudaStream_t s, const int* claim_slots, const ClaimBuf* bufs, int nbuf,
+                   int max_claims) {
+    if (nbuf <= 0 || max_claims <= 0) return;
+    k_claims<<<dim3(max_claims, nbuf), kThreads, 0, s>>>(c, claim_slots, bufs);
+}
+void launch_ring_add(const Ctx& c, cudaStream_t s, PktDev in, BufDev dst) {
+    if (in.halo <= 0) return;
+    const long long n = (2LL * in.halo * (c.cols * in.t + 2 * in.halo) + 2LL * c.rows * in.t * in.halo) * in.C;
+    k_ring_add<<<persistent_grid(n), kThreads, 0, s>>>(c, in, dst);
+}
+void launch_trunc_max(const Ctx& c, cudaStream_t s, PktDev in, BufDev trunc, unsigned* tile_max) {
+    const int nch = chunks_per_tile(in.t, in.C);
+    k_trunc_max<<<c.rows * c.cols * nch, kThreads, 0, s>>>(c, in, trunc, tile_max);
+}
+void launch_trunc_apply(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, const unsigned* tile_max,
+                        float thr, int relu, PktDev out) {
+    const int nch = chunks_per_tile(in.t, in.C);
+    k_trunc_apply<<<c.rows * c.cols * nch, kThreads, 0, s>>>(c, in, acc, trunc, tile_max, thr, relu, out);
+}
+void launch_tile_add(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc) {
+    const int nch = chunks_per_tile(in.t, in.C);
+    k_tile_add<<<c.rows * c.cols * nch, kThreads, 0, s>>>(c, in, acc);
+}
+static int ext_blocks(const Ctx& c, const PktDev& out) { return (c.rows + 2 * out.RT) * (c.cols + 2 * out.RT); }
+void launch_maxpool_out(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, int st, PktDev out,
+                        int hg) {
+    k_maxpool_out<<<ext_blocks(c, out), kThreads, 0, s>>>(c, in, acc, prev, k, st, out, hg);
+}
+void launch_avgpool(const Ctx& c, cudaStream_t s, PktDev in, int k, int st, PktDev out) {
+    k_avgpool<<<ext_blocks(c, out), kThreads, 0, s>>>(c, in, k, st, out);
+}
+void launch_upsample(const Ctx& c, cudaStream_t s, PktDev in, int f, PktDev out) {
+    k_upsample<<<ext_blocks(c, out), kThreads, 0, s>>>(c, in, f, out);
+}
+void launch_bn(const Ctx& c, cudaStream_t s, PktDev in, const float* scale, PktDev out) {
+    k_bn<<<ext_blocks(c, out), kThreads, 0, s>>>(c, in, scale, out);
+}
+void launch_add(const Ctx& c, cudaStream_t s, PktDev a, PktDev b, PktDev out) {
+    k_add<<<ext_blocks(c, out), kThreads, 0, s>>>(c, a, b, out);
+}
+void launch_conv_targets(const Ctx& c, cudaStream_t s, PktDev in, int k, int st, int r, PktDev out, int hg, int* list,
+                         int* count, unsigned long long* flop_px) {
+    const int RTg = (hg + out.t - 1) / out.t;
+    k_conv_targets<<<(c.rows + 2 * RTg) * (c.cols + 2 * RTg), kThreads, 0, s>>>(c, in, k, st, r, out, hg, list, count,
+                                                                                flop_px);
+}
+void launch_conv_exact(const Ctx& c, cudaStream_t s, PktDev in, const float* w, int cin, int cout, int k, int st, int r,
+                       PktDev out, int hg, const int* list, const int* count, int max_targets) {
+    const int K2 = k * k;
+    int ci = 40960 / (4 * K2 * (kXP + kXO));
+    if (ci < 1) ci = 1;
+    if (ci > cin) ci = cin;
+    const size_t smem = (size_t)ci * K2 * (kXP + kXO) * sizeof(float);
+    const long long items = ((long long)(max_targets + kXP - 1) / kXP) * ((cout + kXO - 1) / kXO);
+    long long g = num_sms_cached() * 4;
+    if (items < g) g = items;
+    if (g < 1) g = 1;
+    k_conv_exact<<<(int)g, 256, smem, s>>>(c, in, w, cin, cout, k, st, r, out, hg, list, count, ci);
+}
+void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out) {
+    k_densify<<<persistent_grid((long long)acc.C * c.rows * acc.t * c.cols * acc.t), kThreads, 0, s>>>(c, acc, trunc,
+                                                                                                       out);
+}
+
+}  // namespace dfx

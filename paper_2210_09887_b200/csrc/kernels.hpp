@@ -1,0 +1,78 @@
+// Launch wrappers of the B200 delta-engine kernels (kernels.cu, conv_tc.cu).
+// All take the engine's stream; all per-frame values are read on device from
+// the FrameDev struct, so a frame's launch sequence has fixed shapes.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "dfx_types.hpp"
+
+namespace dfx {
+
+struct Ctx {
+    const FrameDev* f;     // device
+    const SlotDev* slots;  // device [rows*cols]
+    int rows, cols;
+};
+
+struct ClaimBuf {
+    float* d;
+    const float* fill;  // per-channel fill (bias init) or nullptr for zero
+    int C, t;
+};
+
+// ---- input stage (alignment.cpp:58-192, engine.cpp:110-182, 233-234) ----
+void launch_align(const Ctx& c, cudaStream_t s, const float* frame, const float* warped, const uint8_t* fp,
+                  int C, float* aligned, uint8_t* valid, int canvas_pitch, int T);
+void launch_warp(const Ctx& c, cudaStream_t s, const float* frame, int C, float* warped, uint8_t* fp);
+void launch_count_dropped(const Ctx& c, cudaStream_t s, const uint8_t* fp, int T, unsigned long long* counter);
+void launch_roi_factor(const Ctx& c, cudaStream_t s, const float* roi_aligned, float* tmp3, float* fac,
+                       int canvas_pitch, int T);
+void launch_coverage(const Ctx& c, cudaStream_t s, const uint8_t* valid, int canvas_pitch, int T, uint8_t* cov);
+void launch_input_sig(const Ctx& c, cudaStream_t s, const float* aligned, const uint8_t* cov, BufDev acc,
+                      BufDev trunc, const float* fac, float thr, int canvas_pitch, int T, uint8_t* sig);
+void launch_noise(const Ctx& c, cudaStream_t s, const uint8_t* sig, uint8_t* out, int canvas_pitch, int T);
+void launch_gate(const Ctx& c, cudaStream_t s, const uint8_t* sig, const uint8_t* cov, const uint8_t* fresh,
+                 int dilation, int canvas_pitch, int T, uint8_t* gate);
+void launch_input_apply(const Ctx& c, cudaStream_t s, const float* aligned, const uint8_t* cov,
+                        const uint8_t* gate, BufDev acc, BufDev trunc, PktDev out, int canvas_pitch);
+
+// ---- buffer manager (buffer_manager.cpp:68-89, engine.cpp:78-91) ----
+void launch_claims(const Ctx& c, cudaStream_t s, const int* claim_slots, const ClaimBuf* bufs, int nbuf,
+                   int max_claims);
+
+// ---- truncation (delta_layers.cpp:149-232) ----
+void launch_ring_add(const Ctx& c, cudaStream_t s, PktDev in, BufDev dst);
+void launch_trunc_max(const Ctx& c, cudaStream_t s, PktDev in, BufDev trunc, unsigned* tile_max);
+void launch_trunc_apply(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
+                        const unsigned* tile_max, float thr, int relu, PktDev out);
+
+// ---- pooling / linear packet ops (delta_layers.cpp:234-393) ----
+void launch_tile_add(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc);
+void launch_maxpool_out(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, int st,
+                        PktDev out, int out_halo_geom);
+void launch_avgpool(const Ctx& c, cudaStream_t s, PktDev in, int k, int st, PktDev out);
+void launch_upsample(const Ctx& c, cudaStream_t s, PktDev in, int f, PktDev out);
+void launch_bn(const Ctx& c, cudaStream_t s, PktDev in, const float* scale, PktDev out);
+void launch_add(const Ctx& c, cudaStream_t s, PktDev a, PktDev b, PktDev out);
+
+// ---- conv (delta_layers.cpp:100-147) ----
+// Target compaction: writes the compacted target list (packed (y+H)<<16 | (x+H),
+// H = geometric out halo), count (targets in the stored extent) and flops
+// counter (targets in the geometric grown extent), the out ext map, and
+// zeros every non-target pixel of every active out tile.
+void launch_conv_targets(const Ctx& c, cudaStream_t s, PktDev in, int k, int st, int r, PktDev out,
+                         int out_halo_geom, int* list, int* count, unsigned long long* flop_px);
+void launch_conv_exact(const Ctx& c, cudaStream_t s, PktDev in, const float* w, int cin, int cout, int k, int st,
+                       int r, PktDev out, int out_halo_geom, const int* list, const int* count, int max_targets);
+// tcgen05 3xTF32 conv (conv_tc.cu). wsplit: pre-split weights, see conv_tc.cu.
+void launch_conv_tc(const Ctx& c, cudaStream_t s, PktDev in, const float* wsplit, int cin, int cin_pad, int cout,
+                    int cout_pad, int k, int st, int r, PktDev out, int out_halo_geom, const int* list,
+                    const int* count, int max_targets, int num_sms);
+size_t conv_tc_weight_floats(int cin_pad, int cout_pad, int k);
+void conv_tc_prepare_weights(const float* w, int cin, int cout, int k, int cin_pad, int cout_pad, float* out);
+
+// ---- output (delta_layers.cpp:395-400) ----
+void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out);
+
+}  // namespace dfx
