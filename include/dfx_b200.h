@@ -184,9 +184,33 @@ int dfx_engine_read_packet(dfx_engine* e, const char* layer, float* out, size_t 
 int dfx_engine_read_ledger(dfx_engine* e, int* used, int64_t* ty, int64_t* tx, uint8_t* covered,
                            size_t cap);
 
-/* Device work counters of the last frame (for the roofline): number of
- * launches of each kernel family, and algorithmic bytes per family. */
+/* Number of kernels the last frame launched. */
 int dfx_engine_kernel_count(dfx_engine* e);
+
+/* Kernel families for profiling. */
+enum {
+    DFX_FAM_CLAIMS = 0,       /* claim reset + bias init            (HBM)    */
+    DFX_FAM_INPUT = 1,        /* input stage                        (HBM)    */
+    DFX_FAM_CONV_TARGETS = 2, /* conv target compaction + zero fill (HBM)    */
+    DFX_FAM_CONV_MMA = 3,     /* sparse DeltaConv                   (tensor) */
+    DFX_FAM_TRUNC = 4,        /* fused delta activation / truncation (HBM)   */
+    DFX_FAM_POOL = 5,         /* sparse pooling                     (HBM)    */
+    DFX_FAM_LINEAR = 6,       /* upsample / batchnorm / add         (HBM)    */
+    DFX_FAM_DENSIFY = 7,      /* dense output                       (HBM)    */
+    DFX_FAMILIES = 8
+};
+/* Profiling mode: CUDA events around every launch on the engine's stream,
+ * accumulated per family with the family's ALGORITHMIC work (bytes, or conv
+ * FLOPs as the reference's FlopReport counts them). Frames become
+ * synchronous while profiling. */
+int dfx_engine_set_profiling(dfx_engine* e, int on);
+int dfx_engine_reset_profile(dfx_engine* e);
+int dfx_engine_profile(dfx_engine* e, int family, double* ms, uint64_t* launches, double* work);
+const char* dfx_kernel_family_name(int family);
+/* Device timer on the engine's stream (CUDA events): start, then stop
+ * returns the elapsed milliseconds after synchronizing on the stop event. */
+int dfx_engine_timer_start(dfx_engine* e);
+int dfx_engine_timer_stop(dfx_engine* e, float* ms);
 
 void dfx_wrap_tile(int64_t tx, int64_t ty, int rows, int cols, int* row, int* col);
 

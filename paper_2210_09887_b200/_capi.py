@@ -30,6 +30,9 @@ KIND_NAMES = {v: k for k, v in KINDS.items()}
 DFX_OK, DFX_ERR, DFX_ERR_VALIDATION, DFX_ERR_IO, DFX_ERR_CUDA = range(5)
 STATE_ACC, STATE_TRUNC, STATE_PREV = 0, 1, 2
 CONV_TF32X3, CONV_EXACT = 0, 1
+# kernel families (dfx_b200.h DFX_FAM_*); "tensor" families are FLOP-bound, others HBM-bound
+FAMILIES = ["claims_reset", "input_stage", "conv_targets", "conv_mma", "truncate", "pool", "linear_ops", "densify"]
+FAMILY_BOUND = {"conv_mma": "tensor"}
 
 _fp = C.POINTER(C.c_float)
 
@@ -173,10 +176,20 @@ def load_library():
         ("num_layers", C.c_int, [C.c_void_p]),
         ("layer_flops", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         ("kernel_count", C.c_int, [C.c_void_p]),
+        ("set_profiling", C.c_int, [C.c_void_p, C.c_int]),
+        ("reset_profile", C.c_int, [C.c_void_p]),
+        ("profile", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                              C.POINTER(C.c_double)]),
+        ("timer_start", C.c_int, [C.c_void_p]),
+        ("timer_stop", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     ]:
         fn = getattr(lib, f"dfx_engine_{name}")
         fn.restype = res
         fn.argtypes = args
         api[name] = fn
+    fn = lib.dfx_kernel_family_name
+    fn.restype = C.c_char_p
+    fn.argtypes = [C.c_int]
+    api["family_name"] = fn
     _LIB = (lib, api)
     return _LIB

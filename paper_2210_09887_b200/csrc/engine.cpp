@@ -27,6 +27,14 @@ namespace {
 
 thread_local std::string g_err;
 
+#define PROF(fam, call)                \
+    do {                               \
+        const int _pi = prof_begin(fam); \
+        call;                          \
+        prof_end(_pi);                 \
+        ++launches_;                   \
+    } while (0)
+
 #define CUDA_CHECK(x)                                                                                  \
     do {                                                                                               \
         cudaError_t _e = (x);                                                                          \
@@ -139,6 +147,11 @@ class Engine {
     int cols() const { return cols_; }
     int num_layers() const { return (int)net_.layers.size(); }
     int kernel_count() const { return launches_; }
+    void set_profiling(bool on);
+    void profile(int fam, double* ms, uint64_t* launches, double* work) const;
+    void reset_profile();
+    void timer_start();
+    float timer_stop();
 
   private:
     struct LayerRT {
@@ -213,6 +226,22 @@ class Engine {
     dfx_frame_info pending_{};
     bool have_frame_ = false;
     int launches_ = 0;
+    // ---- profiling (per kernel family CUDA events on the engine stream)
+    struct ProfEv {
+        cudaEvent_t a, b;
+        int fam;
+    };
+    bool prof_ = false;
+    std::vector<ProfEv> prof_pool_;
+    size_t prof_used_ = 0;
+    double prof_ms_[DFX_FAMILIES] = {};
+    uint64_t prof_launch_[DFX_FAMILIES] = {};
+    double prof_work_[DFX_FAMILIES] = {};
+    int last_nclaims_ = 0;
+    cudaEvent_t timer_a_ = nullptr, timer_b_ = nullptr;
+    int prof_begin(int fam);
+    void prof_end(int idx);
+    void prof_harvest();
 };
 
 Engine::Engine(const dfx_net_desc* d, const dfx_engine_config* cfg, int device) : cfg_(*cfg), device_(device) {
@@ -232,6 +261,12 @@ Engine::Engine(const dfx_net_desc* d, const dfx_engine_config* cfg, int device) 
 Engine::~Engine() {
     cudaSetDevice(device_);
     if (stream_) cudaStreamSynchronize(stream_);
+    for (auto& e : prof_pool_) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    if (timer_a_) cudaEventDestroy(timer_a_);
+    if (timer_b_) cudaEventDestroy(timer_b_);
     for (int i = 0; i < 2; ++i) {
         if (params_hb_[i]) cudaFreeHost(params_hb_[i]);
         if (params_ev_[i]) cudaEventDestroy(params_ev_[i]);
@@ -435,6 +470,23 @@ void Engine::reset() {
     }
 }
 
+int Engine::prof_begin(int fam) {
+    if (!prof_) return -1;
+    if (prof_used_ == prof_pool_.size()) {
+        ProfEv e{};
+        CUDA_CHECK(cudaEventCreate(&e.a));
+        CUDA_CHECK(cudaEventCreate(&e.b));
+        prof_pool_.push_back(e);
+    }
+    ProfEv& e = prof_pool_[prof_used_];
+    e.fam = fam;
+    CUDA_CHECK(cudaEventRecord(e.a, stream_));
+    return (int)prof_used_++;
+}
+void Engine::prof_end(int idx) {
+    if (idx >= 0) CUDA_CHECK(cudaEventRecord(prof_pool_[idx].b, stream_));
+}
+
 // engine.cpp:184-287 on device.
 void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h9, const float* roi_dev) {
     check(c == net_.in_channels, "run_frame: input channel mismatch");
@@ -507,6 +559,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     F.base_sr = (int)floor_mod64(pl.origin.ty, rows_);
     F.base_sc = (int)floor_mod64(pl.origin.tx, cols_);
     F.nclaims = (int)plan.claims.size();
+    last_nclaims_ = F.nclaims;
     F.frame_h = h;
     F.frame_w = w;
     F.sy0 = sy0;
@@ -546,30 +599,30 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     const int nslots = rows_ * cols_;
 
     // claims reset + implicit bias (buffer_manager.cpp:68-89)
-    launch_claims(C, s, d_claims_, claim_bufs_.p, nclaim_bufs_, max_claims_), ++launches_;
+    PROF(DFX_FAM_CLAIMS, launch_claims(C, s, d_claims_, claim_bufs_.p, nclaim_bufs_, max_claims_));
 
     // input stage
-    if (!integer) launch_warp(C, s, frame_dev, c, warped_d_.p, fp_d_.p), ++launches_;
-    launch_align(C, s, frame_dev, warped_d_.p, fp_d_.p, c, aligned_d_.p, valid_d_.p, canvas_pitch_, T), ++launches_;
-    if (cropped && !integer) launch_count_dropped(C, s, fp_d_.p, T, dropped), ++launches_;
+    if (!integer) PROF(DFX_FAM_INPUT, launch_warp(C, s, frame_dev, c, warped_d_.p, fp_d_.p));
+    PROF(DFX_FAM_INPUT, launch_align(C, s, frame_dev, warped_d_.p, fp_d_.p, c, aligned_d_.p, valid_d_.p, canvas_pitch_, T));
+    if (cropped && !integer) PROF(DFX_FAM_INPUT, launch_count_dropped(C, s, fp_d_.p, T, dropped));
     const float* fac = nullptr;
     if (F.roi) {
-        if (!integer) launch_warp(C, s, roi_dev, 1, roi_warped_d_.p, roi_fp_d_.p), ++launches_;
-        launch_align(C, s, roi_dev, roi_warped_d_.p, roi_fp_d_.p, 1, roi_aligned_d_.p, roi_valid_d_.p, canvas_pitch_, T),
-            ++launches_;
-        launch_roi_factor(C, s, roi_aligned_d_.p, roi_tmp_d_.p, fac_d_.p, canvas_pitch_, T), launches_ += 2;
+        if (!integer) PROF(DFX_FAM_INPUT, launch_warp(C, s, roi_dev, 1, roi_warped_d_.p, roi_fp_d_.p));
+        PROF(DFX_FAM_INPUT, launch_align(C, s, roi_dev, roi_warped_d_.p, roi_fp_d_.p, 1, roi_aligned_d_.p, roi_valid_d_.p, canvas_pitch_, T));
+        PROF(DFX_FAM_INPUT, launch_roi_factor(C, s, roi_aligned_d_.p, roi_tmp_d_.p, fac_d_.p, canvas_pitch_, T));
+        ++launches_;  // two kernels (rows, cols)
         fac = fac_d_.p;
     }
-    launch_coverage(C, s, valid_d_.p, canvas_pitch_, T, cov_d_.p), ++launches_;
-    launch_input_sig(C, s, aligned_d_.p, cov_d_.p, in_acc_, in_trunc_, fac, cfg_.input_threshold, canvas_pitch_, T,
-                     sig_d_.p), ++launches_;
+    PROF(DFX_FAM_INPUT, launch_coverage(C, s, valid_d_.p, canvas_pitch_, T, cov_d_.p));
+    PROF(DFX_FAM_INPUT, launch_input_sig(C, s, aligned_d_.p, cov_d_.p, in_acc_, in_trunc_, fac, cfg_.input_threshold, canvas_pitch_, T,
+                     sig_d_.p));
     const uint8_t* sig = sig_d_.p;
     if (cfg_.noise_suppression) {
-        launch_noise(C, s, sig_d_.p, sig2_d_.p, canvas_pitch_, T), ++launches_;
+        PROF(DFX_FAM_INPUT, launch_noise(C, s, sig_d_.p, sig2_d_.p, canvas_pitch_, T));
         sig = sig2_d_.p;
     }
-    launch_gate(C, s, sig, cov_d_.p, d_fresh_, cfg_.mask_dilation, canvas_pitch_, T, gate_d_.p), ++launches_;
-    launch_input_apply(C, s, aligned_d_.p, cov_d_.p, gate_d_.p, in_acc_, in_trunc_, in_pkt_, canvas_pitch_), ++launches_;
+    PROF(DFX_FAM_INPUT, launch_gate(C, s, sig, cov_d_.p, d_fresh_, cfg_.mask_dilation, canvas_pitch_, T, gate_d_.p));
+    PROF(DFX_FAM_INPUT, launch_input_apply(C, s, aligned_d_.p, cov_d_.p, gate_d_.p, in_acc_, in_trunc_, in_pkt_, canvas_pitch_));
 
     // layers in topological order (engine.cpp:247-281)
     for (int idx2 : net_.topo) {
@@ -578,37 +631,41 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
         const PktDev a = in_packet(l.in0);
         switch (l.kind) {
             case DFX_CONV:
-                launch_conv_targets(C, s, a, l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom, rt.list.p, counts + idx2,
-                                    flop_px + idx2), ++launches_;
+                PROF(DFX_FAM_CONV_TARGETS, launch_conv_targets(C, s, a, l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom, rt.list.p, counts + idx2,
+                                    flop_px + idx2));
+                {
+                const int pi = prof_begin(DFX_FAM_CONV_MMA);
                 if (cfg_.conv_mode == DFX_CONV_EXACT)
                     launch_conv_exact(C, s, a, rt.w.p, l.cin, l.cout, l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom,
                                       rt.list.p, counts + idx2, rt.max_targets);
                 else
                     launch_conv_tc(C, s, a, rt.wtc.p, l.cin, rt.cin_pad, l.cout, rt.cout_pad, l.k, l.stride, l.k / 2,
                                    rt.pkt, rt.halo_geom, rt.list.p, counts + idx2, rt.max_targets, num_sms_);
+                prof_end(pi);
                 ++launches_;
+                }
                 break;
             case DFX_RELU:
             case DFX_TRUNCATE:
             case DFX_OUTPUT:
-                if (a.halo > 0) launch_ring_add(C, s, a, rt.aux), ++launches_;
-                launch_trunc_max(C, s, a, rt.aux, tmax + (size_t)idx2 * nslots), ++launches_;
-                launch_trunc_apply(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots, rt.thr,
-                                   l.kind == DFX_RELU ? 1 : 0, rt.pkt), ++launches_;
+                if (a.halo > 0) PROF(DFX_FAM_TRUNC, launch_ring_add(C, s, a, rt.aux));
+                PROF(DFX_FAM_TRUNC, launch_trunc_max(C, s, a, rt.aux, tmax + (size_t)idx2 * nslots));
+                PROF(DFX_FAM_TRUNC, launch_trunc_apply(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots, rt.thr,
+                                   l.kind == DFX_RELU ? 1 : 0, rt.pkt));
                 break;
             case DFX_MAXPOOL:
-                launch_tile_add(C, s, a, rt.acc), ++launches_;
-                if (a.halo > 0) launch_ring_add(C, s, a, rt.acc), ++launches_;
-                launch_maxpool_out(C, s, a, rt.acc, rt.aux, l.pool_k, l.pool_s, rt.pkt, rt.halo_geom), ++launches_;
+                PROF(DFX_FAM_POOL, launch_tile_add(C, s, a, rt.acc));
+                if (a.halo > 0) PROF(DFX_FAM_POOL, launch_ring_add(C, s, a, rt.acc));
+                PROF(DFX_FAM_POOL, launch_maxpool_out(C, s, a, rt.acc, rt.aux, l.pool_k, l.pool_s, rt.pkt, rt.halo_geom));
                 break;
-            case DFX_AVGPOOL: launch_avgpool(C, s, a, l.pool_k, l.pool_s, rt.pkt), ++launches_; break;
-            case DFX_UPSAMPLE: launch_upsample(C, s, a, l.factor, rt.pkt), ++launches_; break;
-            case DFX_BATCHNORM: launch_bn(C, s, a, rt.scale.p, rt.pkt), ++launches_; break;
-            case DFX_ADD: launch_add(C, s, a, in_packet(l.in1), rt.pkt), ++launches_; break;
+            case DFX_AVGPOOL: PROF(DFX_FAM_POOL, launch_avgpool(C, s, a, l.pool_k, l.pool_s, rt.pkt)); break;
+            case DFX_UPSAMPLE: PROF(DFX_FAM_LINEAR, launch_upsample(C, s, a, l.factor, rt.pkt)); break;
+            case DFX_BATCHNORM: PROF(DFX_FAM_LINEAR, launch_bn(C, s, a, rt.scale.p, rt.pkt)); break;
+            case DFX_ADD: PROF(DFX_FAM_LINEAR, launch_add(C, s, a, in_packet(l.in1), rt.pkt)); break;
         }
     }
     const LayerRT& ort = lrt_[net_.out_layer];
-    launch_densify(C, s, ort.acc, ort.aux, out_d_.p), ++launches_;
+    PROF(DFX_FAM_DENSIFY, launch_densify(C, s, ort.acc, ort.aux, out_d_.p));
     CUDA_CHECK(cudaGetLastError());
 
     // small readback: per-layer target counts, dropped, fired input tiles
@@ -622,6 +679,141 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     info.out_width = tw * ol.in_tile;
     ++frame_index_;
     have_frame_ = true;
+}
+
+void Engine::set_profiling(bool on) {
+    prof_ = on;
+    prof_used_ = 0;
+}
+void Engine::reset_profile() {
+    for (int i = 0; i < DFX_FAMILIES; ++i) prof_ms_[i] = 0, prof_launch_[i] = 0, prof_work_[i] = 0;
+}
+void Engine::profile(int fam, double* ms, uint64_t* launches, double* work) const {
+    check(fam >= 0 && fam < DFX_FAMILIES, "bad kernel family");
+    *ms = prof_ms_[fam];
+    *launches = prof_launch_[fam];
+    *work = prof_work_[fam];
+}
+void Engine::timer_start() {
+    if (!timer_a_) {
+        CUDA_CHECK(cudaEventCreate(&timer_a_));
+        CUDA_CHECK(cudaEventCreate(&timer_b_));
+    }
+    CUDA_CHECK(cudaEventRecord(timer_a_, stream_));
+}
+float Engine::timer_stop() {
+    check(timer_a_ != nullptr, "timer not started");
+    CUDA_CHECK(cudaEventRecord(timer_b_, stream_));
+    CUDA_CHECK(cudaEventSynchronize(timer_b_));
+    float ms = 0;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, timer_a_, timer_b_));
+    return ms;
+}
+
+// Per-family kernel time (CUDA events) and ALGORITHMIC work of the frame
+// (SURVEY §8(d) formulas: bytes for the HBM-bound families, the reference's
+// FlopReport for the convs). Profiling mode only; synchronous.
+void Engine::prof_harvest() {
+    if (!prof_ || prof_used_ == 0) return;
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    for (size_t i = 0; i < prof_used_; ++i) {
+        float ms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, prof_pool_[i].a, prof_pool_[i].b));
+        prof_ms_[prof_pool_[i].fam] += ms;
+        prof_launch_[prof_pool_[i].fam] += 1;
+    }
+    prof_used_ = 0;
+    const int th = place_.th, tw = place_.tw;
+    std::vector<uint8_t> cnt(cnt_bytes_);
+    CUDA_CHECK(cudaMemcpy(cnt.data(), counters_d_.p, cnt_bytes_, cudaMemcpyDeviceToHost));
+    const uint64_t* fpx = reinterpret_cast<const uint64_t*>(cnt.data());
+    const int* counts = reinterpret_cast<const int*>(cnt.data() + off_counts_);
+    auto ext_of = [&](const PktDev& p) {
+        std::vector<uint8_t> e((size_t)(rows_ + 2 * p.RT) * p.ext_pitch);
+        CUDA_CHECK(cudaMemcpy(e.data(), p.ext, e.size(), cudaMemcpyDeviceToHost));
+        return e;
+    };
+    auto inside = [&](const PktDev& p, const std::vector<uint8_t>& e) {
+        double n = 0;
+        for (int r = 0; r < th; ++r)
+            for (int c = 0; c < tw; ++c) n += e[(size_t)(r + p.RT) * p.ext_pitch + c + p.RT] ? 1 : 0;
+        return n;
+    };
+    // valid pixels of the whole grown packet (inside tiles + ring tiles clipped to the grown extent)
+    auto valid_px = [&](const PktDev& p, const std::vector<uint8_t>& e, bool ring_only) {
+        double n = 0;
+        for (int i = -p.RT; i < th + p.RT; ++i)
+            for (int j = -p.RT; j < tw + p.RT; ++j) {
+                const bool in_ext = i >= 0 && i < th && j >= 0 && j < tw;
+                if (ring_only && in_ext) continue;
+                if (!e[(size_t)(i + p.RT) * p.ext_pitch + j + p.RT]) continue;
+                const int y0 = std::max(i * p.t, -p.halo), y1 = std::min((i + 1) * p.t, th * p.t + p.halo);
+                const int x0 = std::max(j * p.t, -p.halo), x1 = std::min((j + 1) * p.t, tw * p.t + p.halo);
+                if (y1 > y0 && x1 > x0) n += (double)(y1 - y0) * (x1 - x0);
+            }
+        return n;
+    };
+    double claim_elems = 0;
+    {
+        std::vector<ClaimBuf> cb(nclaim_bufs_);
+        CUDA_CHECK(cudaMemcpy(cb.data(), claim_bufs_.p, cb.size() * sizeof(ClaimBuf), cudaMemcpyDeviceToHost));
+        for (const auto& b : cb) claim_elems += (double)b.C * b.t * b.t;
+    }
+    prof_work_[DFX_FAM_CLAIMS] += 4.0 * claim_elems * last_nclaims_;
+    {
+        std::vector<uint8_t> cov((size_t)rows_ * cols_);
+        CUDA_CHECK(cudaMemcpy(cov.data(), cov_d_.p, cov.size(), cudaMemcpyDeviceToHost));
+        double ncov = 0;
+        for (int i = 0; i < th * tw; ++i) ncov += cov[i] ? 1 : 0;
+        const double F = inside(in_pkt_, ext_of(in_pkt_));
+        const double T2 = (double)cfg_.tile_size * cfg_.tile_size;
+        prof_work_[DFX_FAM_INPUT] += 4.0 * net_.in_channels * T2 * (3 * ncov + 3 * F + (ncov - F));
+    }
+    for (int idx : net_.topo) {
+        const Layer& l = net_.layers[idx];
+        const LayerRT& rt = lrt_[idx];
+        const PktDev a = in_packet(l.in0);
+        const auto ea = ext_of(a);
+        const auto eo = ext_of(rt.pkt);
+        switch (l.kind) {
+            case DFX_CONV: {
+                const double per_px = 2.0 * l.k * l.k * l.cin * l.cout;
+                prof_work_[DFX_FAM_CONV_MMA] += per_px * (double)fpx[idx];
+                prof_work_[DFX_FAM_CONV_TARGETS] +=
+                    4.0 * l.cout * std::max(0.0, valid_px(rt.pkt, eo, false) - (double)counts[idx]) + 4.0 * counts[idx];
+                break;
+            }
+            case DFX_RELU:
+            case DFX_TRUNCATE:
+            case DFX_OUTPUT: {
+                const double A = inside(a, ea), F = inside(rt.pkt, eo), T2 = (double)a.t * a.t;
+                const double H = a.halo > 0 ? valid_px(a, ea, true) : 0.0;
+                prof_work_[DFX_FAM_TRUNC] += 4.0 * a.C * (T2 * (3 * A + 3 * F) + 3 * H);
+                break;
+            }
+            case DFX_MAXPOOL: {
+                const double A = inside(a, ea), T2 = (double)a.t * a.t;
+                const double H = a.halo > 0 ? valid_px(a, ea, true) : 0.0;
+                prof_work_[DFX_FAM_POOL] += 4.0 * a.C * (3 * A * T2 + 3 * H + 3 * valid_px(rt.pkt, eo, false));
+                break;
+            }
+            case DFX_AVGPOOL:
+                prof_work_[DFX_FAM_POOL] += 4.0 * a.C * (valid_px(a, ea, false) + valid_px(rt.pkt, eo, false));
+                break;
+            case DFX_ADD: {
+                const PktDev b = in_packet(l.in1);
+                prof_work_[DFX_FAM_LINEAR] +=
+                    4.0 * a.C * (valid_px(a, ea, false) + valid_px(b, ext_of(b), false) + valid_px(rt.pkt, eo, false));
+                break;
+            }
+            default:
+                prof_work_[DFX_FAM_LINEAR] += 4.0 * a.C * (valid_px(a, ea, false) + valid_px(rt.pkt, eo, false));
+        }
+    }
+    {
+        const Layer& ol = net_.layers[net_.out_layer];
+        prof_work_[DFX_FAM_DENSIFY] += 12.0 * ol.in_channels * (double)ol.in_tile * ol.in_tile * th * tw;
+    }
 }
 
 void Engine::finish_info(dfx_frame_info* out) {
@@ -678,10 +870,16 @@ void Engine::run_frame(const float* frame, int c, int h, int w, const float* h9,
     CUDA_CHECK(cudaStreamSynchronize(stream_));
     CUDA_CHECK(cudaGetLastError());
     finish_info(info);
+    prof_harvest();
 }
 
 void Engine::submit(const float* frame_dev, int c, int h, int w, const float* h9) {
     CUDA_CHECK(cudaSetDevice(device_));
+    if (prof_ && prof_used_) {
+        CUDA_CHECK(cudaStreamSynchronize(stream_));
+        finish_info(nullptr);
+        prof_harvest();
+    }
     ensure_staging(c, h, w, false);
     enqueue(frame_dev, c, h, w, h9, nullptr);
 }
@@ -692,6 +890,7 @@ void Engine::sync(dfx_frame_info* info) {
     CUDA_CHECK(cudaGetLastError());
     check(have_frame_, "no frame submitted");
     finish_info(info);
+    prof_harvest();
 }
 
 void Engine::output_device(const float** p, int* c, int* h, int* w) const {
@@ -915,6 +1114,26 @@ int dfx_engine_read_ledger(dfx_engine* e, int* used, int64_t* ty, int64_t* tx, u
     return guard([&] { e->e->read_ledger(used, ty, tx, covered, cap); });
 }
 int dfx_engine_kernel_count(dfx_engine* e) { return e->e->kernel_count(); }
+int dfx_engine_set_profiling(dfx_engine* e, int on) {
+    return guard([&] { e->e->set_profiling(on != 0); });
+}
+int dfx_engine_reset_profile(dfx_engine* e) {
+    return guard([&] { e->e->reset_profile(); });
+}
+int dfx_engine_profile(dfx_engine* e, int family, double* ms, uint64_t* launches, double* work) {
+    return guard([&] { e->e->profile(family, ms, launches, work); });
+}
+const char* dfx_kernel_family_name(int family) {
+    static const char* names[DFX_FAMILIES] = {"claims_reset", "input_stage", "conv_targets", "conv_mma",
+                                              "truncate",     "pool",        "linear_ops",   "densify"};
+    return (family >= 0 && family < DFX_FAMILIES) ? names[family] : "?";
+}
+int dfx_engine_timer_start(dfx_engine* e) {
+    return guard([&] { e->e->timer_start(); });
+}
+int dfx_engine_timer_stop(dfx_engine* e, float* ms) {
+    return guard([&] { *ms = e->e->timer_stop(); });
+}
 
 void dfx_wrap_tile(int64_t tx, int64_t ty, int rows, int cols, int* row, int* col) {
     // tile_grid.hpp:37-40

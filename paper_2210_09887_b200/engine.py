@@ -172,7 +172,34 @@ class DeltaEngine:
         return p.value, (c.value, h.value, w.value)
 
     def kernel_count(self) -> int:
+        """Kernels launched by the last frame."""
         return self._api["kernel_count"](self._h)
+
+    # ---- device-side measurement on the engine's stream ----
+    def set_profiling(self, on: bool):
+        _raise(self._api, self._api["set_profiling"](self._h, int(bool(on))))
+
+    def reset_profile(self):
+        _raise(self._api, self._api["reset_profile"](self._h))
+
+    def profile(self) -> dict:
+        """Per kernel family: total ms (CUDA events), launches, algorithmic work
+        (bytes, or FLOPs for conv_mma)."""
+        out = {}
+        for i, name in enumerate(_capi.FAMILIES):
+            ms, n, w = C.c_double(), C.c_uint64(), C.c_double()
+            _raise(self._api, self._api["profile"](self._h, i, C.byref(ms), C.byref(n), C.byref(w)))
+            out[name] = {"ms": ms.value, "launches": n.value, "work": w.value,
+                         "bound": _capi.FAMILY_BOUND.get(name, "hbm")}
+        return out
+
+    def timer_start(self):
+        _raise(self._api, self._api["timer_start"](self._h))
+
+    def timer_stop(self) -> float:
+        ms = C.c_float()
+        _raise(self._api, self._api["timer_stop"](self._h, C.byref(ms)))
+        return ms.value
 
     # ---- introspection (engine.hpp:57-72) ----
     def grid(self):
