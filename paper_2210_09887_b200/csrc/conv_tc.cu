@@ -13,18 +13,19 @@
 // accuracy (|err| ~1e-6 relative), within the stated 1e-4 tolerance of the
 // reference's fp32 outputs.
 //
-// Pipeline (per CTA, persistent over M x N work items), 2 smem stages:
+// Pipeline (per CTA, persistent over M x N work items), 2-4 smem stages:
 //   * B (weights, pre-split hi/lo and pre-laid-out in the UMMA canonical
 //     K-major SWIZZLE_NONE image on the host) arrives by one cp.async.bulk per
-//     stage, completing on an mbarrier with transaction bytes;
-//   * A is gathered by all 256 threads from the HWC delta packet (zero for
+//     stage, completing on the stage's mbarrier with transaction bytes;
+//   * A is gathered by 8 producer warps from the HWC delta packet (zero for
 //     samples outside the packet's written tiles), split hi/lo in registers and
 //     stored in the canonical layout; fence.proxy.async hands it to the tensor
 //     core;
 //   * one thread issues the tcgen05.mma chain and tcgen05.commit's the stage's
-//     mbarrier, so the gather of K-block kb+1 overlaps the MMAs of kb;
-//   * epilogue: tcgen05.ld 32x32b.x32 from TMEM, 128-byte stores of each
-//     pixel's channels into the output packet.
+//     "empty" mbarrier; the producers run up to nstages K-blocks ahead;
+//   * accumulators are double-buffered in TMEM (when 2*N <= 512 columns) so the
+//     4 epilogue warps (tcgen05.ld 32x32b.x32 -> 128-byte stores of each
+//     pixel's channels) drain tile i while the MMAs of tile i+1 run.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -40,7 +41,6 @@ namespace {
 
 constexpr int kM = 128;      // target pixels per tile (MMA M)
 constexpr int kKC = 32;      // input channels per K-block
-constexpr int kThreadsTC = 256;
 constexpr int kAStage = kM * kKC * 4 * 2;  // hi + lo = 32 KiB
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -120,39 +120,78 @@ __device__ __forceinline__ bool valid_px(const PktDev& p, int th, int tw, int y,
     return p.ext[ext_idx(p, floor_div32(y, p.t), floor_div32(x, p.t))] != 0;
 }
 
-__global__ void __launch_bounds__(kThreadsTC, 1)
-    k_conv_tc(Ctx c, PktDev in, const float* __restrict__ wsplit, int cin, int cin_pad, int cout, int cout_pad, int k,
-              int s, int r, PktDev out, int hg, const int* __restrict__ list, const int* __restrict__ count) {
+// Warp roles (416 threads): warps 0-7 are two producer warpgroups that gather
+// A for alternating K-blocks (one thread per row, 32 channels = 8 x 16 B
+// loads, the next K-block of the same group prefetched into registers); warps
+// 8-11 epilogue (TMEM lane quarter = warp % 4); warp 12 issues the MMAs.
+// Barriers: full[s] (4 producer-warp arrivals, the weight bulk copy's
+// transaction bytes), empty[s] (tcgen05.commit), acc_full[b] (commit after a
+// work unit's last K-block), acc_empty[b] (4 epilogue warps).
+// Work unit = (128-row M tile, 256-wide N block, K split). K order: channel
+// block outer, tap inner. Each row's per-tap validity (packet tile written /
+// inside the grown extent) is resolved once per unit into a bitmask, so the
+// K loop issues no dependent loads. Split-K (layers with few target tiles)
+// writes fp32 partials to a workspace reduced in fixed order by
+// k_conv_splitk_reduce (deterministic).
+constexpr int kProdWarps = 8, kEpiWarps = 4;
+constexpr int kThreadsV2 = (kProdWarps + kEpiWarps + 1) * 32;
+
+// expect_tx WITHOUT an arrival (the issuing warp arrives after its own stores)
+__device__ __forceinline__ void mbar_expect_tx_only(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+struct ConvArgs {
+    PktDev in, out;
+    const float* wsplit;
+    const int* list;
+    const int* count;
+    float* ws;  // split-K workspace [splits][n][cout_pad] or nullptr
+    int cin, cin_pad, cout, cout_pad, k, s, r, hg, splits;
+};
+
+template <int NST>
+__global__ void __launch_bounds__(kThreadsV2, 1) k_conv_tc(Ctx c, ConvArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bar_full[2], bar_mma[2];
+    __shared__ __align__(8) uint64_t bar_full[NST], bar_empty[NST], bar_accf[2], bar_acce[2];
     __shared__ uint32_t tmem_base_sh;
-    __shared__ int s_py[kM], s_px[kM];
 
     const FrameDev& F = *c.f;
-    const int n = *count;
-    const int nCB = (cin_pad + kKC - 1) / kKC;
-    const int nKB = k * k * nCB;
-    const int nNB = (cout_pad + 255) / 256;
-    const int items = ((n + kM - 1) / kM) * nNB;
-    if ((int)blockIdx.x >= items) return;
+    const int n = *a.count;
+    const int nCB = (a.cin_pad + kKC - 1) / kKC;
+    const int K2 = a.k * a.k;
+    const int nKB = K2 * nCB;
+    const int nNB = (a.cout_pad + 255) / 256;
+    const int S = a.splits;
+    const int units = ((n + kM - 1) / kM) * nNB * S;
+    if ((int)blockIdx.x >= units) return;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int NBmax = cout_pad < 256 ? cout_pad : 256;
-    const uint32_t b_stage_bytes = (uint32_t)NBmax * kKC * 4 * 2;
+    const int NBmax = a.cout_pad < 256 ? a.cout_pad : 256;
+    const uint32_t b_stage_bytes = (uint32_t)NBmax * kKC * 8;
     const uint32_t stage_bytes = kAStage + b_stage_bytes;
-    uint32_t ncols = 32;
-    while ((int)ncols < NBmax) ncols <<= 1;
+    uint32_t acc_cols = 32;
+    while ((int)acc_cols < NBmax) acc_cols <<= 1;
+    const int nbuf = acc_cols * 2 <= 512 ? 2 : 1;
+    const uint32_t ncols = acc_cols * nbuf;
 
-    if (warp == 0) {
+    if (warp == kProdWarps + kEpiWarps) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
                      "r"(ncols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        mbar_init(smem_u32(&bar_full[0]), 1);
-        mbar_init(smem_u32(&bar_full[1]), 1);
-        mbar_init(smem_u32(&bar_mma[0]), 1);
-        mbar_init(smem_u32(&bar_mma[1]), 1);
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(smem_u32(&bar_full[i]), 4);
+            mbar_init(smem_u32(&bar_empty[i]), 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&bar_accf[i]), 1);
+            mbar_init(smem_u32(&bar_acce[i]), kEpiWarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc_fence_before();
@@ -161,126 +200,223 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint32_t tmem = tmem_base_sh;
     const uint32_t smem_base = smem_u32(smem);
 
-    const int row = tid & (kM - 1), half = tid >> 7;  // gather: 2 threads per row, 16 channels each
-    uint32_t g = 0;                                   // global K-block counter (stage / parity bookkeeping)
+    // unit -> (m tile, n block, split) and its K-block range
+    auto unit_info = [&](int u, int& mb, int& nb, int& kb0, int& kb1) {
+        const int sp = u % S, t = u / S;
+        mb = t / nNB;
+        nb = t % nNB;
+        kb0 = (int)(((long long)nKB * sp) / S);
+        kb1 = (int)(((long long)nKB * (sp + 1)) / S);
+    };
 
-    for (int item = blockIdx.x; item < items; item += gridDim.x) {
-        const int mb = item / nNB, nb = item % nNB;
-        const int NB = (cout_pad - nb * 256) < 256 ? (cout_pad - nb * 256) : 256;
-        const uint32_t idesc = idesc_tf32(NB);
-        if (tid < kM) {
-            const int idx = mb * kM + tid;
+    if (warp < kProdWarps) {
+        // ------------------------------------------------ producers
+        const int wg = warp >> 2;      // warpgroup: K-blocks with g % 2 == wg
+        const int row = tid & (kM - 1);
+        const int wid_in_wg = warp & 3;
+        // state of the K-block this thread gathers next
+        int u = blockIdx.x, mb, nb, kb0, kb1;
+        unit_info(u, mb, nb, kb0, kb1);
+        int kb = kb0;
+        uint32_t g = 0;  // CTA-global K-block sequence number of (u, kb)
+        int py = 0, px = 0;
+        uint64_t vmask = 0;
+        auto load_rows = [&]() {
+            const int idx = mb * kM + row;
+            py = -(1 << 20), px = -(1 << 20);
+            vmask = 0;
             if (idx < n) {
-                const int v = list[idx];
-                s_py[tid] = (v >> 16) - hg;
-                s_px[tid] = (v & 0xffff) - hg;
+                const int v = __ldg(a.list + idx);
+                py = (v >> 16) - a.hg;
+                px = (v & 0xffff) - a.hg;
+                for (int tp = 0; tp < K2; ++tp) {
+                    const int ky = tp / a.k, kx = tp - ky * a.k;
+                    if (valid_px(a.in, F.th, F.tw, py * a.s - a.r + ky, px * a.s - a.r + kx)) vmask |= 1ull << tp;
+                }
+            }
+        };
+        auto advance = [&]() {  // move (u, kb, g) one K-block forward in the CTA sequence
+            ++g;
+            if (++kb == kb1) {
+                u += gridDim.x;
+                if (u < units) {
+                    unit_info(u, mb, nb, kb0, kb1);
+                    kb = kb0;
+                    load_rows();
+                }
+            }
+        };
+        auto gather = [&](float* v) {
+            const int cb = kb / K2, tap = kb - cb * K2;
+            const int ky = tap / a.k, kx = tap - ky * a.k;
+            const int cbeg = cb * kKC;
+            const bool ok = (vmask >> tap) & 1ull;
+            if (ok && (a.in.C & 3) == 0 && cbeg + kKC <= a.cin) {
+                const float4* src = reinterpret_cast<const float4*>(
+                    a.in.d + pkt_off(a.in, py * a.s - a.r + ky, px * a.s - a.r + kx) + cbeg);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float4 t = __ldg(src + j);
+                    v[4 * j] = t.x, v[4 * j + 1] = t.y, v[4 * j + 2] = t.z, v[4 * j + 3] = t.w;
+                }
             } else {
-                s_py[tid] = -(1 << 20);
-                s_px[tid] = -(1 << 20);
+                const float* src = ok ? a.in.d + pkt_off(a.in, py * a.s - a.r + ky, px * a.s - a.r + kx) : nullptr;
+#pragma unroll
+                for (int j = 0; j < kKC; ++j) v[j] = (ok && cbeg + j < a.cin) ? __ldg(src + cbeg + j) : 0.0f;
             }
-        }
-        __syncthreads();
-        const int py = s_py[row], px = s_px[row];
-        const float* wblk = wsplit + (size_t)nb * 256 * nKB * kKC * 2;
-
-        for (int kb = 0; kb < nKB; ++kb, ++g) {
-            const uint32_t st = g & 1, q = g >> 1;
+        };
+        load_rows();
+        if (wg == 1) advance();  // warpgroup 1 starts at the second K-block
+        float cur[kKC];
+        bool have = u < units;
+        if (have) gather(cur);
+        while (have) {
+            const uint32_t my_g = g;
+            const int my_kb = kb, my_nb = nb;
+            // prefetch this warpgroup's next K-block (two ahead in the CTA sequence)
+            advance();
+            if (u < units) advance();
+            const bool has_next = u < units;
+            float nxt[kKC];
+            if (has_next) gather(nxt);
+            const uint32_t st = my_g % NST, q = my_g / NST;
+            const int NB = (a.cout_pad - my_nb * 256) < 256 ? (a.cout_pad - my_nb * 256) : 256;
+            mbar_wait(smem_u32(&bar_empty[st]), (q & 1) ^ 1);
             const uint32_t a_base = smem_base + st * stage_bytes;
-            const uint32_t b_base = a_base + kAStage;
-            if (g >= 2) mbar_wait(smem_u32(&bar_mma[st]), (q - 1) & 1);
-            const int tap = kb / nCB, cb = kb - tap * nCB;
-            const int c0 = cb * kKC;
-            if (tid == 0) {
-                mbar_expect_tx(smem_u32(&bar_full[st]), (uint32_t)NB * kKC * 8);
-                bulk_g2s(b_base, wblk + (size_t)kb * NB * kKC * 2, (uint32_t)NB * kKC * 8, smem_u32(&bar_full[st]));
+            if (wid_in_wg == 0 && lane == 0) {
+                const float* wblk = a.wsplit + (size_t)my_nb * 256 * nKB * kKC * 2;
+                mbar_expect_tx_only(smem_u32(&bar_full[st]), (uint32_t)NB * kKC * 8);
+                bulk_g2s(a_base + kAStage, wblk + (size_t)my_kb * NB * kKC * 2, (uint32_t)NB * kKC * 8,
+                         smem_u32(&bar_full[st]));
             }
-            // ---- gather + split A (rows = target pixels, K = 32 channels at this tap)
-            {
-                float v[16];
-                const int ky = tap / k, kx = tap - ky * k;
-                const int iy = py * s - r + ky, ix = px * s - r + kx;
-                const int cbeg = c0 + half * 16;
-                const bool ok = py > -(1 << 19) && valid_px(in, F.th, F.tw, iy, ix);
-                if (ok && (in.C & 3) == 0 && cbeg + 16 <= cin) {
-                    const float4* src = reinterpret_cast<const float4*>(in.d + pkt_off(in, iy, ix) + cbeg);
+            uint8_t* a_hi = smem + st * stage_bytes;
+            uint8_t* a_lo = a_hi + kM * kKC * 4;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const float4 t = __ldg(src + j);
-                        v[4 * j] = t.x, v[4 * j + 1] = t.y, v[4 * j + 2] = t.z, v[4 * j + 3] = t.w;
-                    }
-                } else {
-                    const float* src = ok ? in.d + pkt_off(in, iy, ix) : nullptr;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = (ok && cbeg + j < cin) ? src[cbeg + j] : 0.0f;
-                }
-                uint8_t* a_hi = smem + st * stage_bytes;
-                uint8_t* a_lo = a_hi + kM * kKC * 4;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    uint4 hi, lo;
-                    hi.x = to_tf32(v[4 * j]);
-                    hi.y = to_tf32(v[4 * j + 1]);
-                    hi.z = to_tf32(v[4 * j + 2]);
-                    hi.w = to_tf32(v[4 * j + 3]);
-                    lo.x = to_tf32(__fsub_rn(v[4 * j], __uint_as_float(hi.x)));
-                    lo.y = to_tf32(__fsub_rn(v[4 * j + 1], __uint_as_float(hi.y)));
-                    lo.z = to_tf32(__fsub_rn(v[4 * j + 2], __uint_as_float(hi.z)));
-                    lo.w = to_tf32(__fsub_rn(v[4 * j + 3], __uint_as_float(hi.w)));
-                    const int kc = half * 4 + j;  // 16-byte K chunk within the block
-                    const uint32_t off = (uint32_t)kc * (kM * 16) + (uint32_t)row * 16;
-                    *reinterpret_cast<uint4*>(a_hi + off) = hi;
-                    *reinterpret_cast<uint4*>(a_lo + off) = lo;
-                }
+            for (int j = 0; j < 8; ++j) {
+                uint4 hi, lo;
+                hi.x = to_tf32(cur[4 * j]);
+                hi.y = to_tf32(cur[4 * j + 1]);
+                hi.z = to_tf32(cur[4 * j + 2]);
+                hi.w = to_tf32(cur[4 * j + 3]);
+                lo.x = to_tf32(__fsub_rn(cur[4 * j], __uint_as_float(hi.x)));
+                lo.y = to_tf32(__fsub_rn(cur[4 * j + 1], __uint_as_float(hi.y)));
+                lo.z = to_tf32(__fsub_rn(cur[4 * j + 2], __uint_as_float(hi.z)));
+                lo.w = to_tf32(__fsub_rn(cur[4 * j + 3], __uint_as_float(hi.w)));
+                const uint32_t off = (uint32_t)j * (kM * 16) + (uint32_t)row * 16;
+                *reinterpret_cast<uint4*>(a_hi + off) = hi;
+                *reinterpret_cast<uint4*>(a_lo + off) = lo;
             }
             fence_proxy_async();
-            __syncthreads();
-            if (tid == 0) {
-                mbar_wait(smem_u32(&bar_full[st]), q & 1);
-                tc_fence_after();
-                const int nsteps = (cin_pad - c0) / 8 < 4 ? (cin_pad - c0) / 8 : 4;
-                const uint32_t lbo_a = kM * 16, lbo_b = (uint32_t)NB * 16;
-                for (int j = 0; j < nsteps; ++j) {
-                    const uint64_t dah = umma_desc(a_base + 2 * j * lbo_a, lbo_a, 128);
-                    const uint64_t dal = umma_desc(a_base + kM * kKC * 4 + 2 * j * lbo_a, lbo_a, 128);
-                    const uint64_t dbh = umma_desc(b_base + 2 * j * lbo_b, lbo_b, 128);
-                    const uint64_t dbl = umma_desc(b_base + (uint32_t)NB * kKC * 4 + 2 * j * lbo_b, lbo_b, 128);
-                    mma_tf32(tmem, dal, dbh, idesc, (kb > 0 || j > 0) ? 1u : 0u);
-                    mma_tf32(tmem, dah, dbl, idesc, 1u);
-                    mma_tf32(tmem, dah, dbh, idesc, 1u);
-                }
-                mma_commit(smem_u32(&bar_mma[st]));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bar_full[st]));
+            have = has_next;
+            if (have) {
+#pragma unroll
+                for (int j = 0; j < kKC; ++j) cur[j] = nxt[j];
             }
         }
-        // ---- epilogue: wait for the last commit (covers all earlier MMAs)
-        {
-            const uint32_t gl = g - 1;
-            mbar_wait(smem_u32(&bar_mma[gl & 1]), (gl >> 1) & 1);
+    } else if (warp < kProdWarps + kEpiWarps) {
+        // ------------------------------------------------ epilogue: TMEM -> packet / workspace
+        const int lq = warp & 3;
+        uint32_t ui = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++ui) {
+            int mb, nb, kb0, kb1;
+            unit_info(u, mb, nb, kb0, kb1);
+            const int NB = (a.cout_pad - nb * 256) < 256 ? (a.cout_pad - nb * 256) : 256;
+            const uint32_t b = nbuf == 2 ? (ui & 1) : 0, ub = nbuf == 2 ? (ui >> 1) : ui;
+            mbar_wait(smem_u32(&bar_accf[b]), ub & 1);
             tc_fence_after();
-            const int lq = warp & 3, chalf = warp >> 2;
-            const int prow = lq * 32 + lane;
-            const int oy = s_py[prow], ox = s_px[prow];
-            const bool valid = oy > -(1 << 19);
-            for (int cc = chalf * 32; cc < NB; cc += 64) {
+            const int idx = mb * kM + lq * 32 + lane;
+            const bool valid = idx < n;
+            float* dst_row = nullptr;
+            int lim = a.cout;
+            if (valid) {
+                if (S > 1) {
+                    dst_row = a.ws + ((size_t)(u % S) * n + idx) * a.cout_pad;
+                    lim = a.cout_pad;
+                } else {
+                    const int v = __ldg(a.list + idx);
+                    dst_row = a.out.d + pkt_off(a.out, (v >> 16) - a.hg, (v & 0xffff) - a.hg);
+                }
+            }
+            for (int cc = 0; cc < NB; cc += 32) {
                 float v[32];
-                tmem_ld32(tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)cc, v);
+                tmem_ld32(tmem + b * acc_cols + ((uint32_t)(lq * 32) << 16) + (uint32_t)cc, v);
                 if (valid) {
                     const int o0 = nb * 256 + cc;
-                    float* dst = out.d + pkt_off(out, oy, ox) + o0;
-                    if ((out.C & 3) == 0 && o0 + 32 <= cout) {
+                    float* dst = dst_row + o0;
+                    if (((S > 1) || (a.out.C & 3) == 0) && o0 + 32 <= lim) {
 #pragma unroll
                         for (int j = 0; j < 8; ++j)
                             reinterpret_cast<float4*>(dst)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
                     } else {
-                        for (int j = 0; j < 32 && o0 + j < cout; ++j) dst[j] = v[j];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (o0 + j < lim) dst[j] = v[j];
                     }
                 }
             }
             tc_fence_before();
-            __syncthreads();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bar_acce[b]));
         }
+    } else {
+        // ------------------------------------------------ MMA issuer (one thread)
+        if (lane == 0) {
+            uint32_t g = 0, ui = 0;
+            const uint32_t lbo_a = kM * 16;
+            for (int u = blockIdx.x; u < units; u += gridDim.x, ++ui) {
+                int mb, nb, kb0, kb1;
+                unit_info(u, mb, nb, kb0, kb1);
+                const int NB = (a.cout_pad - nb * 256) < 256 ? (a.cout_pad - nb * 256) : 256;
+                const uint32_t idesc = idesc_tf32(NB);
+                const uint32_t lbo_b = (uint32_t)NB * 16;
+                const uint32_t b = nbuf == 2 ? (ui & 1) : 0, ub = nbuf == 2 ? (ui >> 1) : ui;
+                mbar_wait(smem_u32(&bar_acce[b]), (ub & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dtm = tmem + b * acc_cols;
+                for (int kb = kb0; kb < kb1; ++kb, ++g) {
+                    const uint32_t st = g % NST, q = g / NST;
+                    mbar_wait(smem_u32(&bar_full[st]), q & 1);
+                    tc_fence_after();
+                    const int c0 = (kb / K2) * kKC;
+                    const int nsteps = (a.cin_pad - c0) / 8 < 4 ? (a.cin_pad - c0) / 8 : 4;
+                    const uint32_t a_base = smem_base + st * stage_bytes, b_base = a_base + kAStage;
+                    for (int j = 0; j < nsteps; ++j) {
+                        const uint64_t dah = umma_desc(a_base + 2 * j * lbo_a, lbo_a, 128);
+                        const uint64_t dal = umma_desc(a_base + kM * kKC * 4 + 2 * j * lbo_a, lbo_a, 128);
+                        const uint64_t dbh = umma_desc(b_base + 2 * j * lbo_b, lbo_b, 128);
+                        const uint64_t dbl = umma_desc(b_base + (uint32_t)NB * kKC * 4 + 2 * j * lbo_b, lbo_b, 128);
+                        mma_tf32(dtm, dal, dbh, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
+                        mma_tf32(dtm, dah, dbl, idesc, 1u);
+                        mma_tf32(dtm, dah, dbh, idesc, 1u);
+                    }
+                    mma_commit(smem_u32(&bar_empty[st]));
+                }
+                mma_commit(smem_u32(&bar_accf[b]));
+            }
+        }
+        __syncwarp();
     }
+    tc_fence_before();
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
+    tc_fence_after();
+    if (warp == kProdWarps + kEpiWarps)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
+}
+
+// Fixed-order split-K reduction into the output packet (deterministic).
+__global__ void k_conv_splitk_reduce(ConvArgs a) {
+    const int n = *a.count;
+    const long long total = (long long)n * a.cout;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int idx = (int)(e / a.cout), o = (int)(e % a.cout);
+        float sum = a.ws[(size_t)idx * a.cout_pad + o];
+        for (int sp = 1; sp < a.splits; ++sp) sum = __fadd_rn(sum, a.ws[((size_t)sp * n + idx) * a.cout_pad + o]);
+        const int v = __ldg(a.list + idx);
+        a.out.d[pkt_off(a.out, (v >> 16) - a.hg, (v & 0xffff) - a.hg) + o] = sum;
+    }
 }
 
 uint32_t rna_tf32_host(float x) {
@@ -307,7 +443,7 @@ void conv_tc_prepare_weights(const float* w, int cin, int cout, int k, int cin_p
         const int NB = std::min(256, cout_pad - nb * 256);
         float* base = outp + (size_t)nb * 256 * nKB * kKC * 2;
         for (int kb = 0; kb < nKB; ++kb) {
-            const int tap = kb / nCB, cb = kb % nCB;
+            const int cb = kb / K2, tap = kb % K2;
             float* blob = base + (size_t)kb * NB * kKC * 2;
             for (int nn = 0; nn < NB; ++nn) {
                 const int o = nb * 256 + nn;
@@ -330,23 +466,52 @@ void conv_tc_prepare_weights(const float* w, int cin, int cout, int k, int cin_p
     }
 }
 
+int conv_tc_splits(int max_targets, int cin_pad, int cout_pad, int k, int num_sms) {
+    const int nCB = (cin_pad + kKC - 1) / kKC, nKB = k * k * nCB;
+    const int nNB = (cout_pad + 255) / 256;
+    const long long tiles = (long long)((max_targets + kM - 1) / kM) * nNB;
+    // split K when the layer cannot give every SM a tile; keep >= 4 K-blocks per split
+    int S = 1;
+    while (tiles * S * 2 <= num_sms && nKB / (S * 2) >= 4 && S < 16) S *= 2;
+    return S;
+}
+
+template <int NST>
+static void launch_nst(int grid, size_t smem, cudaStream_t s, const Ctx& c, const ConvArgs& a) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_conv_tc<NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = true;
+    }
+    k_conv_tc<NST><<<grid, kThreadsV2, smem, s>>>(c, a);
+}
+
 void launch_conv_tc(const Ctx& c, cudaStream_t s, PktDev in, const float* wsplit, int cin, int cin_pad, int cout,
                     int cout_pad, int k, int st, int r, PktDev out, int hg, const int* list, const int* count,
-                    int max_targets, int num_sms) {
+                    int max_targets, int num_sms, float* ws, int splits) {
     const int NBmax = cout_pad < 256 ? cout_pad : 256;
-    const size_t smem = 2 * ((size_t)kAStage + (size_t)NBmax * kKC * 8);
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = 200 * 1024;
-    }
-    if (smem > 200 * 1024) throw std::runtime_error("conv_tc: smem too large");
+    const size_t stage = (size_t)kAStage + (size_t)NBmax * kKC * 8;
+    const size_t budget = 200 * 1024;
+    int nstages = (int)(budget / stage);
+    if (nstages > 4) nstages = 4;
+    if (nstages < 2) throw std::runtime_error("conv_tc: Cout too large for two pipeline stages");
+    if (k * k > 64) throw std::runtime_error("conv_tc: kernel larger than 7x7 is not supported");
+    ConvArgs a{in, out, wsplit, list, count, splits > 1 ? ws : nullptr, cin, cin_pad, cout, cout_pad, k, st, r, hg,
+               splits > 1 ? splits : 1};
     const int nNB = (cout_pad + 255) / 256;
-    const long long items = (long long)((max_targets + kM - 1) / kM) * nNB;
+    const long long units = (long long)((max_targets + kM - 1) / kM) * nNB * a.splits;
     int grid = num_sms;
-    if (items < grid) grid = (int)(items < 1 ? 1 : items);
-    k_conv_tc<<<grid, kThreadsTC, smem, s>>>(c, in, wsplit, cin, cin_pad, cout, cout_pad, k, st, r, out, hg, list,
-                                             count);
+    if (units < grid) grid = (int)(units < 1 ? 1 : units);
+    const size_t smem = nstages * stage;
+    if (nstages == 4) launch_nst<4>(grid, smem, s, c, a);
+    else if (nstages == 3) launch_nst<3>(grid, smem, s, c, a);
+    else launch_nst<2>(grid, smem, s, c, a);
+    if (a.splits > 1) {
+        long long total = (long long)max_targets * cout;
+        int rg = (int)((total + 255) / 256);
+        if (rg > num_sms * 8) rg = num_sms * 8;
+        k_conv_splitk_reduce<<<rg < 1 ? 1 : rg, 256, 0, s>>>(a);
+    }
 }
 
 }  // namespace dfx

@@ -170,6 +170,8 @@ class Engine {
         int cin_pad = 0, cout_pad = 0;
         DevArr<int> list;
         int max_targets = 0;
+        int splits = 1;
+        DevArr<float> ws;
     };
 
     void allocate(int th, int tw);
@@ -341,6 +343,7 @@ void Engine::allocate(int th, int tw) {
         const int hin = l.in0 == -1 ? 0 : lrt_[l.in0].halo_store;
         switch (l.kind) {
             case DFX_CONV: {
+                check(l.tile <= 64, "conv output tile larger than 64 px is not supported by the target kernel");
                 rt.halo_geom = windowed_out_halo(hin, l.k, l.k / 2, l.stride);
                 rt.halo_store = cfg_.padded_convolutions ? rt.halo_geom : 0;
                 build_packet(rt, l.cout, l.tile, rt.halo_store);
@@ -355,6 +358,8 @@ void Engine::allocate(int th, int tw) {
                     conv_tc_prepare_weights(l.w.data(), l.cin, l.cout, l.k, rt.cin_pad, rt.cout_pad, ws.data());
                     rt.wtc.alloc(ws.size());
                     CUDA_CHECK(cudaMemcpy(rt.wtc.p, ws.data(), ws.size() * 4, cudaMemcpyHostToDevice));
+                    rt.splits = conv_tc_splits(rt.max_targets, rt.cin_pad, rt.cout_pad, l.k, num_sms_);
+                    if (rt.splits > 1) rt.ws.alloc((size_t)rt.splits * rt.max_targets * rt.cout_pad);
                 }
                 break;
             }
@@ -640,7 +645,8 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                                       rt.list.p, counts + idx2, rt.max_targets);
                 else
                     launch_conv_tc(C, s, a, rt.wtc.p, l.cin, rt.cin_pad, l.cout, rt.cout_pad, l.k, l.stride, l.k / 2,
-                                   rt.pkt, rt.halo_geom, rt.list.p, counts + idx2, rt.max_targets, num_sms_);
+                                   rt.pkt, rt.halo_geom, rt.list.p, counts + idx2, rt.max_targets, num_sms_, rt.ws.p,
+                                   rt.splits);
                 prof_end(pi);
                 ++launches_;
                 }
@@ -649,14 +655,26 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
             case DFX_TRUNCATE:
             case DFX_OUTPUT:
                 if (a.halo > 0) PROF(DFX_FAM_TRUNC, launch_ring_add(C, s, a, rt.aux));
-                PROF(DFX_FAM_TRUNC, launch_trunc_max(C, s, a, rt.aux, tmax + (size_t)idx2 * nslots));
-                PROF(DFX_FAM_TRUNC, launch_trunc_apply(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots, rt.thr,
-                                   l.kind == DFX_RELU ? 1 : 0, rt.pkt));
+                {
+                    bool fused = false;
+                    PROF(DFX_FAM_TRUNC, fused = launch_trunc_fused(C, s, a, rt.acc, rt.aux, rt.thr,
+                                                                  l.kind == DFX_RELU ? 1 : 0, rt.pkt));
+                    if (!fused) {
+                        --launches_;
+                        PROF(DFX_FAM_TRUNC, launch_trunc_max(C, s, a, rt.aux, tmax + (size_t)idx2 * nslots));
+                        PROF(DFX_FAM_TRUNC, launch_trunc_apply(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots,
+                                                             rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt));
+                    }
+                }
                 break;
             case DFX_MAXPOOL:
-                PROF(DFX_FAM_POOL, launch_tile_add(C, s, a, rt.acc));
-                if (a.halo > 0) PROF(DFX_FAM_POOL, launch_ring_add(C, s, a, rt.acc));
-                PROF(DFX_FAM_POOL, launch_maxpool_out(C, s, a, rt.acc, rt.aux, l.pool_k, l.pool_s, rt.pkt, rt.halo_geom));
+                if (a.halo == 0 && l.pool_k == l.pool_s) {
+                    PROF(DFX_FAM_POOL, launch_maxpool_fused(C, s, a, rt.acc, rt.aux, l.pool_k, rt.pkt));
+                } else {
+                    PROF(DFX_FAM_POOL, launch_tile_add(C, s, a, rt.acc));
+                    if (a.halo > 0) PROF(DFX_FAM_POOL, launch_ring_add(C, s, a, rt.acc));
+                    PROF(DFX_FAM_POOL, launch_maxpool_out(C, s, a, rt.acc, rt.aux, l.pool_k, l.pool_s, rt.pkt, rt.halo_geom));
+                }
                 break;
             case DFX_AVGPOOL: PROF(DFX_FAM_POOL, launch_avgpool(C, s, a, l.pool_k, l.pool_s, rt.pkt)); break;
             case DFX_UPSAMPLE: PROF(DFX_FAM_LINEAR, launch_upsample(C, s, a, l.factor, rt.pkt)); break;

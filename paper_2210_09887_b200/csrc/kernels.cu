@@ -489,6 +489,116 @@ __global__ void k_trunc_apply(Ctx c, PktDev in, BufDev acc, BufDev trunc, const 
     }
 }
 
+// Fused delta activation, one HBM pass per tile (delta_layers.cpp:185-228):
+// a CTA (or a cluster of cs CTAs for large tiles) loads the tile's trunc and
+// delta once into registers, reduces max|trunc + delta| (cross-CTA through
+// DSMEM), then fires (acc += cand, trunc = 0, out = relu(acc') - relu(acc))
+// or folds (trunc += delta) straight from registers. Requires C % 4 == 0 and
+// t*t*C <= cs * kTruncThreads * 4 * kTruncVec.
+constexpr int kTruncThreads = 512, kTruncVec = 8;
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float ld_dsmem_f32(const float* local, uint32_t rank) {
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(local), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kTruncThreads, 1)
+    k_trunc_fused(Ctx c, PktDev in, BufDev acc, BufDev trunc, float thr, int relu, PktDev out, int cs) {
+    __shared__ float red[32];
+    __shared__ float s_blockmax;
+    const FrameDev& F = *c.f;
+    const int T = in.t, C = in.C;
+    const int ti = blockIdx.x / cs;
+    const uint32_t rank = cs > 1 ? cluster_rank() : 0;
+    // uniform per cluster: every CTA of the cluster handles the same tile
+    if (ti >= F.th * F.tw) return;
+    const int tr = ti / F.tw, tc = ti % F.tw;
+    const bool masked = in.ext[ext_idx(in, tr, tc)] && holds(c, F, tr, tc);
+    if (!masked) {
+        if (rank == 0 && threadIdx.x == 0) out.ext[ext_idx(out, tr, tc)] = 0;
+        return;
+    }
+    const int E4 = T * T * C / 4;              // float4s in the tile
+    const int per = (E4 + cs - 1) / cs;         // float4s of this CTA
+    const int q0 = rank * per, q1 = min(E4, q0 + per);
+    const int row4 = T * C / 4;                 // float4s per tile row
+    float4* tb = reinterpret_cast<float4*>(tile_ptr(c, F, trunc, tr, tc));
+    float4 tv[kTruncVec], dv[kTruncVec];
+    float m = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kTruncVec; ++j) {
+        const int q = q0 + threadIdx.x + j * kTruncThreads;
+        if (q < q1) {
+            const int yy = q / row4, rem = q - yy * row4;
+            tv[j] = tb[q];
+            dv[j] = reinterpret_cast<const float4*>(in.d + pkt_off(in, tr * T + yy, tc * T))[rem];
+            m = fmaxf(m, fabsf(__fadd_rn(tv[j].x, dv[j].x)));
+            m = fmaxf(m, fabsf(__fadd_rn(tv[j].y, dv[j].y)));
+            m = fmaxf(m, fabsf(__fadd_rn(tv[j].z, dv[j].z)));
+            m = fmaxf(m, fabsf(__fadd_rn(tv[j].w, dv[j].w)));
+        }
+    }
+    m = block_max(m, red);
+    if (cs > 1) {
+        if (threadIdx.x == 0) s_blockmax = m;
+        cluster_sync_all();
+        float mm = 0.0f;
+        for (int r = 0; r < cs; ++r) mm = fmaxf(mm, ld_dsmem_f32(&s_blockmax, r));
+        m = mm;
+        cluster_sync_all();  // remote reads done before any CTA of the cluster exits
+    }
+    const bool fire = m >= thr && m > 0.0f;
+    if (rank == 0 && threadIdx.x == 0) out.ext[ext_idx(out, tr, tc)] = fire ? 1 : 0;
+    if (fire) {
+        float4* ab = reinterpret_cast<float4*>(tile_ptr(c, F, acc, tr, tc));
+#pragma unroll
+        for (int j = 0; j < kTruncVec; ++j) {
+            const int q = q0 + threadIdx.x + j * kTruncThreads;
+            if (q < q1) {
+                const int yy = q / row4, rem = q - yy * row4;
+                const float4 pv = ab[q];
+                float4 cd, nv, o;
+                cd.x = __fadd_rn(tv[j].x, dv[j].x); cd.y = __fadd_rn(tv[j].y, dv[j].y);
+                cd.z = __fadd_rn(tv[j].z, dv[j].z); cd.w = __fadd_rn(tv[j].w, dv[j].w);
+                nv.x = __fadd_rn(pv.x, cd.x); nv.y = __fadd_rn(pv.y, cd.y);
+                nv.z = __fadd_rn(pv.z, cd.z); nv.w = __fadd_rn(pv.w, cd.w);
+                if (relu) {
+                    o.x = __fsub_rn(fmaxf(nv.x, 0.f), fmaxf(pv.x, 0.f));
+                    o.y = __fsub_rn(fmaxf(nv.y, 0.f), fmaxf(pv.y, 0.f));
+                    o.z = __fsub_rn(fmaxf(nv.z, 0.f), fmaxf(pv.z, 0.f));
+                    o.w = __fsub_rn(fmaxf(nv.w, 0.f), fmaxf(pv.w, 0.f));
+                } else {
+                    o = cd;
+                }
+                ab[q] = nv;
+                tb[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                reinterpret_cast<float4*>(out.d + pkt_off(out, tr * T + yy, tc * T))[rem] = o;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kTruncVec; ++j) {
+            const int q = q0 + threadIdx.x + j * kTruncThreads;
+            if (q < q1) {
+                float4 nt;
+                nt.x = __fadd_rn(tv[j].x, dv[j].x); nt.y = __fadd_rn(tv[j].y, dv[j].y);
+                nt.z = __fadd_rn(tv[j].z, dv[j].z); nt.w = __fadd_rn(tv[j].w, dv[j].w);
+                tb[q] = nt;
+            }
+        }
+    }
+}
+
 // acc += delta on masked owned tiles (delta_layers.cpp:253-261).
 __global__ void k_tile_add(Ctx c, PktDev in, BufDev acc) {
     const FrameDev& F = *c.f;
@@ -546,59 +656,165 @@ __device__ __forceinline__ void tile_px_range(const FrameDev& F, const PktDev& o
 // Conv target compaction + output ext map + zero fill of non-targets.
 // Iterates the GEOMETRIC grown extent (out_halo_geom) so FLOPs count ring
 // targets even when the stored packet is cropped (padded_convolutions=false,
-// engine.cpp:254-264).
-__global__ void k_conv_targets(Ctx c, PktDev in, int k, int s, int r, PktDev out, int hg, int* __restrict__ list,
-                               int* __restrict__ count, unsigned long long* __restrict__ flop_px) {
-    __shared__ int s_cnt, s_base;
+// engine.cpp:254-264). One block per extended output tile: the input-tile
+// neighbourhood the tile's windows can reach is staged in shared memory, each
+// pixel's target bit is computed once into a shared bitmap, the list is
+// appended with one global atomic per warp (ballot + popc), and non-target
+// pixels of active tiles are zeroed with 16-byte stores.
+constexpr int kTgtMaxPx = 4096;  // t_out <= 64
+__global__ void __launch_bounds__(256) k_conv_targets(Ctx c, PktDev in, int k, int s, int r, PktDev out, int hg,
+                                                      int* __restrict__ list, int* __restrict__ count,
+                                                      unsigned long long* __restrict__ flop_px) {
+    __shared__ uint32_t s_bits[kTgtMaxPx / 32];
+    __shared__ uint8_t s_nb[8][8];
+    __shared__ int s_tr0, s_tc0;
     const FrameDev& F = *c.f;
-    const int RTg = (hg + out.t - 1) / out.t;
+    const int t = out.t;
+    const int RTg = (hg + t - 1) / t;
     const int ew = F.tw + 2 * RTg;
     const int b = blockIdx.x;
     if (b >= (F.th + 2 * RTg) * ew) return;
     const int i = b / ew - RTg, j = b % ew - RTg;
-    const int t = out.t;
-    // geometric range
     const int gy0 = max(i * t, -hg), gy1 = min((i + 1) * t, F.th * t + hg);
     const int gx0 = max(j * t, -hg), gx1 = min((j + 1) * t, F.tw * t + hg);
     const bool stored_tile = i >= -out.RT && i < F.th + out.RT && j >= -out.RT && j < F.tw + out.RT;
-    if (threadIdx.x == 0) s_cnt = 0;
+    // input tiles reachable from this output tile's windows
+    const int ry0 = gy0 * s - r - in.halo, ry1 = (gy1 - 1) * s - r + k - 1 + in.halo;
+    const int rx0 = gx0 * s - r - in.halo, rx1 = (gx1 - 1) * s - r + k - 1 + in.halo;
+    const int tr0 = floor_div32(ry0, in.t), tr1 = floor_div32(ry1, in.t);
+    const int tc0 = floor_div32(rx0, in.t), tc1 = floor_div32(rx1, in.t);
+    const bool nb_ok = (tr1 - tr0) < 8 && (tc1 - tc0) < 8;
+    if (threadIdx.x < 64) {
+        const int a = threadIdx.x >> 3, bb = threadIdx.x & 7;
+        const int tr = tr0 + a, tc = tc0 + bb;
+        uint8_t v = 0;
+        if (tr <= tr1 && tc <= tc1 && tr >= 0 && tr < F.th && tc >= 0 && tc < F.tw) v = in.ext[ext_idx(in, tr, tc)];
+        s_nb[a][bb] = v;
+    }
+    if (threadIdx.x == 0) s_tr0 = tr0, s_tc0 = tc0;
     __syncthreads();
     const int w = gx1 - gx0, n = (gy1 - gy0) * w;
-    int geo_targets = 0, any_stored = 0;
-    for (int p = threadIdx.x; p < n; p += blockDim.x) {
-        const int oy = gy0 + p / w, ox = gx0 + p % w;
-        if (is_target(in, F.th, F.tw, oy, ox, k, r, s)) {
-            ++geo_targets;
-            if (oy >= -out.halo && oy < F.th * t + out.halo && ox >= -out.halo && ox < F.tw * t + out.halo)
-                any_stored = 1;
+    int geo = 0, any_stored = 0;
+    for (int p0 = 0; p0 < n; p0 += blockDim.x) {
+        const int p = p0 + threadIdx.x;
+        bool tgt = false;
+        if (p < n) {
+            const int oy = gy0 + p / w, ox = gx0 + p % w;
+            if (nb_ok) {
+                const int a0 = floor_div32(oy * s - r - in.halo, in.t) - s_tr0;
+                const int a1 = floor_div32(oy * s - r + k - 1 + in.halo, in.t) - s_tr0;
+                const int b0 = floor_div32(ox * s - r - in.halo, in.t) - s_tc0;
+                const int b1 = floor_div32(ox * s - r + k - 1 + in.halo, in.t) - s_tc0;
+                for (int a = a0; a <= a1 && !tgt; ++a)
+                    for (int bb = b0; bb <= b1; ++bb)
+                        if (s_nb[a][bb]) {
+                            tgt = true;
+                            break;
+                        }
+            } else {
+                tgt = is_target(in, F.th, F.tw, oy, ox, k, r, s);
+            }
+            if (tgt) {
+                ++geo;
+                if (oy >= -out.halo && oy < F.th * t + out.halo && ox >= -out.halo && ox < F.tw * t + out.halo)
+                    any_stored = 1;
+            }
         }
+        const unsigned m = __ballot_sync(0xffffffffu, tgt);
+        if ((threadIdx.x & 31) == 0 && p0 + (threadIdx.x & ~31) < kTgtMaxPx)
+            s_bits[(p0 + (threadIdx.x & ~31)) >> 5] = m;
     }
+    for (int o = 16; o > 0; o >>= 1) geo += __shfl_xor_sync(0xffffffffu, geo, o);
+    if ((threadIdx.x & 31) == 0 && geo) atomicAdd(flop_px, (unsigned long long)geo);
     any_stored = __syncthreads_or(any_stored);
-    if (geo_targets) atomicAdd(flop_px, (unsigned long long)geo_targets);
     if (stored_tile && threadIdx.x == 0) out.ext[ext_idx(out, i, j)] = any_stored ? 1 : 0;
     if (!stored_tile || !any_stored) return;
-    int y0, y1, x0, x1;
-    tile_px_range(F, out, i, j, y0, y1, x0, x1);
+    // stored pixel range of this tile
+    const int y0 = max(i * t, -out.halo), y1 = min((i + 1) * t, F.th * t + out.halo);
+    const int x0 = max(j * t, -out.halo), x1 = min((j + 1) * t, F.tw * t + out.halo);
+    auto bit = [&](int oy, int ox) {
+        const int p = (oy - gy0) * w + (ox - gx0);
+        return (s_bits[p >> 5] >> (p & 31)) & 1u;
+    };
     const int sw = x1 - x0, sn = (y1 - y0) * sw;
-    // pass 1: count + zero non-targets
-    for (int p = threadIdx.x; p < sn; p += blockDim.x) {
-        const int oy = y0 + p / sw, ox = x0 + p % sw;
-        if (is_target(in, F.th, F.tw, oy, ox, k, r, s)) {
-            atomicAdd(&s_cnt, 1);
-        } else {
-            float* d = out.d + pkt_off(out, oy, ox);
-            for (int ch = 0; ch < out.C; ++ch) d[ch] = 0.0f;
+    // list append: one atomic per warp
+    for (int p0 = 0; p0 < sn; p0 += blockDim.x) {
+        const int p = p0 + threadIdx.x;
+        int oy = 0, ox = 0;
+        bool tgt = false;
+        if (p < sn) {
+            oy = y0 + p / sw;
+            ox = x0 + p % sw;
+            tgt = bit(oy, ox);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, tgt);
+        int base = 0;
+        if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(count, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (tgt) list[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = ((oy + hg) << 16) | (ox + hg);
+    }
+    // zero fill non-targets
+    const int C = out.C;
+    if ((C & 3) == 0) {
+        const int c4 = C >> 2;
+        for (int e = threadIdx.x; e < sn * c4; e += blockDim.x) {
+            const int p = e / c4, q = e - p * c4;
+            const int oy = y0 + p / sw, ox = x0 + p % sw;
+            if (!bit(oy, ox)) reinterpret_cast<float4*>(out.d + pkt_off(out, oy, ox))[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    } else {
+        for (int e = threadIdx.x; e < sn * C; e += blockDim.x) {
+            const int p = e / C, q = e - p * C;
+            const int oy = y0 + p / sw, ox = x0 + p % sw;
+            if (!bit(oy, ox)) out.d[pkt_off(out, oy, ox) + q] = 0.0f;
         }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) s_base = atomicAdd(count, s_cnt), s_cnt = 0;
-    __syncthreads();
-    for (int p = threadIdx.x; p < sn; p += blockDim.x) {
-        const int oy = y0 + p / sw, ox = x0 + p % sw;
-        if (is_target(in, F.th, F.tw, oy, ox, k, r, s)) {
-            const int slot = s_base + atomicAdd(&s_cnt, 1);
-            list[slot] = ((oy + hg) << 16) | (ox + hg);
+}
+
+// Max pool, halo-free input and k == stride (the engine's only pooling shape,
+// network.cpp:164-166): every output pixel's window lies inside the input tile
+// with the same tile coordinates, so fold (acc += delta, delta_layers.cpp:
+// 253-261) and the window max / prev update (:277-317) fuse into ONE pass over
+// each masked tile. Targets == all pixels of masked tiles; ownership of the
+// input and output tile is the same slot.
+__global__ void k_maxpool_fused(Ctx c, PktDev in, BufDev acc, BufDev prev, int k, PktDev out) {
+    const FrameDev& F = *c.f;
+    const int to = out.t, ti_ = in.t, C = in.C;
+    const int per_tile = to * to * C;
+    const int chunk = 4096;
+    const int nch = (per_tile + chunk - 1) / chunk;
+    const int tix = blockIdx.x / nch, ch = blockIdx.x % nch;
+    if (tix >= F.th * F.tw) return;
+    const int tr = tix / F.tw, tc = tix % F.tw;
+    const bool masked = in.ext[ext_idx(in, tr, tc)] != 0;
+    if (ch == 0 && threadIdx.x == 0) out.ext[ext_idx(out, tr, tc)] = masked ? 1 : 0;
+    if (!masked) return;
+    const bool owned = holds(c, F, tr, tc);
+    const int e0 = ch * chunk, e1 = min(per_tile, e0 + chunk);
+    float* ab = owned ? tile_ptr(c, F, acc, tr, tc) : nullptr;
+    float* pb = owned ? tile_ptr(c, F, prev, tr, tc) : nullptr;
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const int px = e / C, chn = e - px * C;
+        const int y = px / to, x = px - y * to;
+        float* d = out.d + pkt_off(out, tr * to + y, tc * to + x) + chn;
+        if (!owned) {
+            *d = 0.0f;
+            continue;
         }
+        float m = 0.0f;
+        bool first = true;
+        for (int ky = 0; ky < k; ++ky)
+            for (int kx = 0; kx < k; ++kx) {
+                const int iy = y * k + ky, ix = x * k + kx;
+                const size_t ai = ((size_t)iy * ti_ + ix) * C + chn;
+                const float v = __fadd_rn(ab[ai], in.d[pkt_off(in, tr * ti_ + iy, tc * ti_ + ix) + chn]);
+                ab[ai] = v;
+                m = first ? v : fmaxf(m, v);
+                first = false;
+            }
+        float* pv = pb + ((size_t)y * to + x) * C + chn;
+        *d = __fsub_rn(m, *pv);
+        *pv = m;
     }
 }
 
@@ -902,6 +1118,27 @@ void launch_trunc_apply(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, Buf
     const int nch = chunks_per_tile(in.t, in.C);
     k_trunc_apply<<<c.rows * c.cols * nch, kThreads, 0, s>>>(c, in, acc, trunc, tile_max, thr, relu, out);
 }
+bool launch_trunc_fused(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, float thr, int relu,
+                        PktDev out) {
+    const long long E4 = (long long)in.t * in.t * in.C / 4;
+    if ((in.C & 3) != 0) return false;
+    const long long per_cta = (long long)kTruncThreads * kTruncVec;
+    int cs = 1;
+    while (cs * per_cta < E4) cs <<= 1;
+    if (cs > 8) return false;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c.rows * c.cols * cs);
+    cfg.blockDim = dim3(kTruncThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = cs > 1 ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_trunc_fused, c, in, acc, trunc, thr, relu, out, cs) == cudaSuccess;
+}
 void launch_tile_add(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc) {
     const int nch = chunks_per_tile(in.t, in.C);
     k_tile_add<<<c.rows * c.cols * nch, kThreads, 0, s>>>(c, in, acc);
@@ -910,6 +1147,10 @@ static int ext_blocks(const Ctx& c, const PktDev& out) { return (c.rows + 2 * ou
 void launch_maxpool_out(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, int st, PktDev out,
                         int hg) {
     k_maxpool_out<<<ext_blocks(c, out), kThreads, 0, s>>>(c, in, acc, prev, k, st, out, hg);
+}
+void launch_maxpool_fused(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, PktDev out) {
+    const int nch = (out.t * out.t * in.C + 4095) / 4096;
+    k_maxpool_fused<<<c.rows * c.cols * nch, kThreads, 0, s>>>(c, in, acc, prev, k, out);
 }
 void launch_avgpool(const Ctx& c, cudaStream_t s, PktDev in, int k, int st, PktDev out) {
     k_avgpool<<<ext_blocks(c, out), kThreads, 0, s>>>(c, in, k, st, out);

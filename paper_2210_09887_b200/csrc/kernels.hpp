@@ -44,6 +44,10 @@ void launch_claims(const Ctx& c, cudaStream_t s, const int* claim_slots, const C
 // ---- truncation (delta_layers.cpp:149-232) ----
 void launch_ring_add(const Ctx& c, cudaStream_t s, PktDev in, BufDev dst);
 void launch_trunc_max(const Ctx& c, cudaStream_t s, PktDev in, BufDev trunc, unsigned* tile_max);
+// One-pass fused truncation (register-resident tile, DSMEM max across a
+// cluster); returns false when the shape needs the two-pass fallback.
+bool launch_trunc_fused(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, float thr, int relu,
+                        PktDev out);
 void launch_trunc_apply(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
                         const unsigned* tile_max, float thr, int relu, PktDev out);
 
@@ -51,6 +55,8 @@ void launch_trunc_apply(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, Buf
 void launch_tile_add(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc);
 void launch_maxpool_out(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, int st,
                         PktDev out, int out_halo_geom);
+// Fused fold + window max for halo-free inputs with k == stride.
+void launch_maxpool_fused(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, PktDev out);
 void launch_avgpool(const Ctx& c, cudaStream_t s, PktDev in, int k, int st, PktDev out);
 void launch_upsample(const Ctx& c, cudaStream_t s, PktDev in, int f, PktDev out);
 void launch_bn(const Ctx& c, cudaStream_t s, PktDev in, const float* scale, PktDev out);
@@ -66,9 +72,12 @@ void launch_conv_targets(const Ctx& c, cudaStream_t s, PktDev in, int k, int st,
 void launch_conv_exact(const Ctx& c, cudaStream_t s, PktDev in, const float* w, int cin, int cout, int k, int st,
                        int r, PktDev out, int out_halo_geom, const int* list, const int* count, int max_targets);
 // tcgen05 3xTF32 conv (conv_tc.cu). wsplit: pre-split weights, see conv_tc.cu.
+// splits > 1: split-K over `splits` parts into the fp32 workspace ws
+// ([splits][max_targets][cout_pad]) + a fixed-order reduction (deterministic).
 void launch_conv_tc(const Ctx& c, cudaStream_t s, PktDev in, const float* wsplit, int cin, int cin_pad, int cout,
                     int cout_pad, int k, int st, int r, PktDev out, int out_halo_geom, const int* list,
-                    const int* count, int max_targets, int num_sms);
+                    const int* count, int max_targets, int num_sms, float* ws, int splits);
+int conv_tc_splits(int max_targets, int cin_pad, int cout_pad, int k, int num_sms);
 size_t conv_tc_weight_floats(int cin_pad, int cout_pad, int k);
 void conv_tc_prepare_weights(const float* w, int cin, int cout, int k, int cin_pad, int cout_pad, float* out);
 
