@@ -97,6 +97,27 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t 
         "l"(da), "l"(db), "r"(idesc), "r"(acc)
         : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem desc]
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                            uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]),
+        "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),
+        "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -171,12 +192,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1) k_conv_tc(Ctx c, ConvArgs a) {
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int NBmax = a.cout_pad < 256 ? a.cout_pad : 256;
-    const uint32_t b_stage_bytes = (uint32_t)NBmax * kKC * 8;
-    const uint32_t stage_bytes = kAStage + b_stage_bytes;
+    const uint32_t stage_bytes = (uint32_t)NBmax * kKC * 8;  // smem: weights only
+    // TMEM (512 columns): accumulators [0, nbuf*acc_cols), then NST A stages of
+    // 64 columns (32 hi + 32 lo tf32 columns per row / lane).
     uint32_t acc_cols = 32;
     while ((int)acc_cols < NBmax) acc_cols <<= 1;
-    const int nbuf = acc_cols * 2 <= 512 ? 2 : 1;
-    const uint32_t ncols = acc_cols * nbuf;
+    const int nbuf = acc_cols * 2 + NST * 64 <= 512 ? 2 : 1;
+    const uint32_t ncols = 512;
+    const uint32_t a_col0 = nbuf * acc_cols;
 
     if (warp == kProdWarps + kEpiWarps) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
@@ -282,31 +305,25 @@ __global__ void __launch_bounds__(kThreadsV2, 1) k_conv_tc(Ctx c, ConvArgs a) {
             const uint32_t st = my_g % NST, q = my_g / NST;
             const int NB = (a.cout_pad - my_nb * 256) < 256 ? (a.cout_pad - my_nb * 256) : 256;
             mbar_wait(smem_u32(&bar_empty[st]), (q & 1) ^ 1);
-            const uint32_t a_base = smem_base + st * stage_bytes;
+            tc_fence_after();
+            const uint32_t b_base = smem_base + st * stage_bytes;
             if (wid_in_wg == 0 && lane == 0) {
                 const float* wblk = a.wsplit + (size_t)my_nb * 256 * nKB * kKC * 2;
                 mbar_expect_tx_only(smem_u32(&bar_full[st]), (uint32_t)NB * kKC * 8);
-                bulk_g2s(a_base + kAStage, wblk + (size_t)my_kb * NB * kKC * 2, (uint32_t)NB * kKC * 8,
-                         smem_u32(&bar_full[st]));
+                bulk_g2s(b_base, wblk + (size_t)my_kb * NB * kKC * 2, (uint32_t)NB * kKC * 8, smem_u32(&bar_full[st]));
             }
-            uint8_t* a_hi = smem + st * stage_bytes;
-            uint8_t* a_lo = a_hi + kM * kKC * 4;
+            {
+                uint32_t part[kKC];
+                const uint32_t taddr = tmem + ((uint32_t)(wid_in_wg * 32) << 16) + a_col0 + st * 64;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                uint4 hi, lo;
-                hi.x = to_tf32(cur[4 * j]);
-                hi.y = to_tf32(cur[4 * j + 1]);
-                hi.z = to_tf32(cur[4 * j + 2]);
-                hi.w = to_tf32(cur[4 * j + 3]);
-                lo.x = to_tf32(__fsub_rn(cur[4 * j], __uint_as_float(hi.x)));
-                lo.y = to_tf32(__fsub_rn(cur[4 * j + 1], __uint_as_float(hi.y)));
-                lo.z = to_tf32(__fsub_rn(cur[4 * j + 2], __uint_as_float(hi.z)));
-                lo.w = to_tf32(__fsub_rn(cur[4 * j + 3], __uint_as_float(hi.w)));
-                const uint32_t off = (uint32_t)j * (kM * 16) + (uint32_t)row * 16;
-                *reinterpret_cast<uint4*>(a_hi + off) = hi;
-                *reinterpret_cast<uint4*>(a_lo + off) = lo;
+                for (int j = 0; j < kKC; ++j) part[j] = to_tf32(cur[j]);
+                tmem_st32(taddr, part);
+#pragma unroll
+                for (int j = 0; j < kKC; ++j) part[j] = to_tf32(__fsub_rn(cur[j], __uint_as_float(to_tf32(cur[j]))));
+                tmem_st32(taddr + 32, part);
             }
-            fence_proxy_async();
+            tmem_wait_st();
+            tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&bar_full[st]));
             have = has_next;
@@ -364,7 +381,6 @@ __global__ void __launch_bounds__(kThreadsV2, 1) k_conv_tc(Ctx c, ConvArgs a) {
         // ------------------------------------------------ MMA issuer (one thread)
         if (lane == 0) {
             uint32_t g = 0, ui = 0;
-            const uint32_t lbo_a = kM * 16;
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++ui) {
                 int mb, nb, kb0, kb1;
                 unit_info(u, mb, nb, kb0, kb1);
@@ -381,15 +397,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1) k_conv_tc(Ctx c, ConvArgs a) {
                     tc_fence_after();
                     const int c0 = (kb / K2) * kKC;
                     const int nsteps = (a.cin_pad - c0) / 8 < 4 ? (a.cin_pad - c0) / 8 : 4;
-                    const uint32_t a_base = smem_base + st * stage_bytes, b_base = a_base + kAStage;
+                    const uint32_t b_base = smem_base + st * stage_bytes;
+                    const uint32_t a_tm = tmem + a_col0 + st * 64;
                     for (int j = 0; j < nsteps; ++j) {
-                        const uint64_t dah = umma_desc(a_base + 2 * j * lbo_a, lbo_a, 128);
-                        const uint64_t dal = umma_desc(a_base + kM * kKC * 4 + 2 * j * lbo_a, lbo_a, 128);
                         const uint64_t dbh = umma_desc(b_base + 2 * j * lbo_b, lbo_b, 128);
                         const uint64_t dbl = umma_desc(b_base + (uint32_t)NB * kKC * 4 + 2 * j * lbo_b, lbo_b, 128);
-                        mma_tf32(dtm, dal, dbh, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
-                        mma_tf32(dtm, dah, dbl, idesc, 1u);
-                        mma_tf32(dtm, dah, dbh, idesc, 1u);
+                        mma_tf32_ts(dtm, a_tm + 32 + 8 * j, dbh, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
+                        mma_tf32_ts(dtm, a_tm + 8 * j, dbl, idesc, 1u);
+                        mma_tf32_ts(dtm, a_tm + 8 * j, dbh, idesc, 1u);
                     }
                     mma_commit(smem_u32(&bar_empty[st]));
                 }
@@ -490,10 +505,15 @@ void launch_conv_tc(const Ctx& c, cudaStream_t s, PktDev in, const float* wsplit
                     int cout_pad, int k, int st, int r, PktDev out, int hg, const int* list, const int* count,
                     int max_targets, int num_sms, float* ws, int splits) {
     const int NBmax = cout_pad < 256 ? cout_pad : 256;
-    const size_t stage = (size_t)kAStage + (size_t)NBmax * kKC * 8;
+    const size_t stage = (size_t)NBmax * kKC * 8;
     const size_t budget = 200 * 1024;
     int nstages = (int)(budget / stage);
     if (nstages > 4) nstages = 4;
+    {
+        int acc = 32;
+        while (acc < NBmax) acc <<= 1;
+        while (nstages > 2 && acc + nstages * 64 > 512) --nstages;  // TMEM: acc + A stages
+    }
     if (nstages < 2) throw std::runtime_error("conv_tc: Cout too large for two pipeline stages");
     if (k * k > 64) throw std::runtime_error("conv_tc: kernel larger than 7x7 is not supported");
     ConvArgs a{in, out, wsplit, list, count, splits > 1 ? ws : nullptr, cin, cin_pad, cout, cout_pad, k, st, r, hg,
