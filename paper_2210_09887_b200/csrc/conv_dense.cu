@@ -1,0 +1,817 @@
+// Dense-unit sparse DeltaConv on tcgen05 (sm_100a): the bulk of a stride-1
+// padded_delta_conv (reference src/delta_layers.cpp:100-147).
+//
+// The conv output extent is cut into UNITS of 16 rows x 8 columns = 128 output
+// pixels = one MMA M tile. k_conv_units marks a unit DENSE when at least half
+// of its in-extent pixels are conv targets (delta_layers.cpp:34-70); dense
+// units are computed here, every other target (sparse units, the grown ring
+// outside the extent) by the gathered kernel in conv_tc.cu. Both write
+// disjoint pixels of the output packet.
+//
+// Why whole units are exact: a non-target pixel's window touches no masked
+// input tile (grown by the input halo), and unmasked packet tiles are zero by
+// definition (delta_layers.hpp:37-41), so computing it yields exactly the 0
+// the reference stores there; target pixels get the full window sum.
+//
+// Data movement: per (unit, 32-channel chunk) the (16+2r) x (8+2r) input patch
+// is copied ONCE into shared memory with cp.async (zero-fill via src-size 0
+// for samples outside the grown extent or in unwritten tiles), laid out
+// [c4][py][px][4 ch] — exactly the UMMA canonical K-major SWIZZLE_NONE image
+// with 8-pixel rows as core-matrix rows. Every tap (ky, kx) is then the same
+// patch seen through a descriptor whose start address moves by
+// (ky * PW + kx) * 16 bytes (SBO = PW * 16 bytes between unit rows): no
+// per-tap gathers, and the TF32 hi/lo split is done once per patch instead of
+// once per tap. Weights (pre-split hi/lo, per (N-block, K-block) images) are
+// streamed by one thread with cp.async.bulk into a stage ring.
+//
+// Arithmetic: 3xTF32 (Ahi*Bhi + Ahi*Blo + Alo*Bhi, fp32 accumulation in TMEM),
+// the same as conv_tc.cu. Split-K over CTAs (deep layers with few units)
+// writes fp32 partials reduced in fixed order (deterministic).
+//
+// Warp roles (320 threads): 0-3 patch producers, 4-7 epilogue (TMEM lane
+// quarter = warp % 4), 8 weight producer, 9 MMA issuer. Two units share each
+// weight stage (M = 256 rows per weight byte; weight streaming from L2 is the
+// per-SM limit at M = 128).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <stdexcept>
+
+#include "kernels.hpp"
+
+namespace dfx {
+
+namespace {
+
+constexpr int kUY = 16, kUX = 8;  // unit = 16 rows x 8 cols = 128 pixels
+constexpr int kThreads = 320;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+__device__ __forceinline__ uint32_t idesc_tf32(int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ bool pkt_ok(const PktDev& p, int th, int tw, int y, int x) {
+    if (y < -p.halo || y >= th * p.t + p.halo || x < -p.halo || x >= tw * p.t + p.halo) return false;
+    return p.ext[ext_idx(p, floor_div32(y, p.t), floor_div32(x, p.t))] != 0;
+}
+
+// Target test of a stride-1 window (delta_layers.cpp:34-45, :60-70).
+__device__ __forceinline__ bool is_target_s1(const PktDev& in, int th, int tw, int oy, int ox, int k, int r) {
+    const int iy0 = oy - r - in.halo, iy1 = oy - r + k - 1 + in.halo;
+    const int ix0 = ox - r - in.halo, ix1 = ox - r + k - 1 + in.halo;
+    const int tr0 = max(floor_div32(iy0, in.t), 0), tr1 = min(floor_div32(iy1, in.t), th - 1);
+    const int tc0 = max(floor_div32(ix0, in.t), 0), tc1 = min(floor_div32(ix1, in.t), tw - 1);
+    for (int tr = tr0; tr <= tr1; ++tr)
+        for (int tc = tc0; tc <= tc1; ++tc)
+            if (in.ext[ext_idx(in, tr, tc)]) return true;
+    return false;
+}
+
+// Conv planning for the dense path (replaces target compaction for stride-1
+// convs; delta_layers.cpp:34-83). One CTA per BLOCK = the union of whole units
+// and whole tiles: a tile when t >= 16 (t/16 x t/8 units), a unit when t < 16
+// (16/t x 8/t tiles). Blocks are aligned at pixel (0, 0); block row/col 0 is
+// the one above/left of the extent, so the grown ring [-hg, 0) is covered.
+// Per block: the target bit of every pixel of the geometric grown extent
+// (FLOPs count all of them, :139-145), the exact output TileMask / ext byte of
+// every stored tile (any target inside the stored extent, :72-83), every unit
+// with >= 1 target appended to the dense list (units encoded
+// (uy + 1) << 16 | (ux + 1)), and zeros for the pixels of active stored tiles
+// that no dense unit covers (possible only when a tile holds several units).
+constexpr int kPlanThreads = 256;
+__global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, PktDev out, int k, int r, int hg,
+                                                            int nbw, int* __restrict__ units,
+                                                            int* __restrict__ nunits,
+                                                            unsigned long long* __restrict__ flop_px) {
+    __shared__ uint32_t s_bits[4096 / 32];
+    __shared__ int s_ucnt[32];
+    __shared__ int s_tstore[32];
+    const FrameDev& F = *c.f;
+    const int t = out.t;
+    const int BH = t > kUY ? t : kUY, BW = t > kUX ? t : kUX;
+    const int by = blockIdx.x / nbw, bx = blockIdx.x - (blockIdx.x / nbw) * nbw;
+    const int Y0 = (by - 1) * BH, X0 = (bx - 1) * BW;
+    const int eh = F.th * t, ew = F.tw * t;
+    const int hs = out.halo;
+    // block entirely outside the grown extent: nothing to do (its tiles are beyond ext)
+    if (Y0 >= eh + hg || X0 >= ew + hg || Y0 + BH <= -hg || X0 + BW <= -hg) return;
+    const int upr = BW / kUX, nun = (BH / kUY) * upr;  // units in block
+    const int tpr = BW / t, ntl = (BH / t) * tpr;        // tiles in block
+    if (threadIdx.x < 32) {
+        s_ucnt[threadIdx.x] = 0;
+        s_tstore[threadIdx.x] = 0;
+    }
+    __syncthreads();
+    const int npx = BH * BW;
+    int geo = 0;
+    for (int p0 = 0; p0 < npx; p0 += kPlanThreads) {
+        const int p = p0 + threadIdx.x;
+        bool tgt = false;
+        if (p < npx) {
+            const int ly = p / BW, lx = p - (p / BW) * BW;
+            const int y = Y0 + ly, x = X0 + lx;
+            if (y >= -hg && y < eh + hg && x >= -hg && x < ew + hg) tgt = is_target_s1(in, F.th, F.tw, y, x, k, r);
+            if (tgt) {
+                ++geo;
+                atomicAdd(&s_ucnt[(ly / kUY) * upr + lx / kUX], 1);
+                if (y >= -hs && y < eh + hs && x >= -hs && x < ew + hs) s_tstore[(ly / t) * tpr + lx / t] = 1;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, tgt);
+        if ((threadIdx.x & 31) == 0 && p < npx) s_bits[p >> 5] = m;
+    }
+    for (int o = 16; o > 0; o >>= 1) geo += __shfl_xor_sync(0xffffffffu, geo, o);
+    if ((threadIdx.x & 31) == 0 && geo) atomicAdd(flop_px, (unsigned long long)geo);
+    __syncthreads();
+    if (threadIdx.x < nun && s_ucnt[threadIdx.x] > 0) {
+        const int uy = Y0 / kUY + threadIdx.x / upr, ux = X0 / kUX + threadIdx.x % upr;
+        units[atomicAdd(nunits, 1)] = ((uy + 1) << 16) | (ux + 1);
+    }
+    if (threadIdx.x < ntl) {
+        const int ti = floor_div32(Y0, t) + threadIdx.x / tpr, tj = floor_div32(X0, t) + threadIdx.x % tpr;
+        if (ti >= -out.RT && ti < F.th + out.RT && tj >= -out.RT && tj < F.tw + out.RT)
+            out.ext[ext_idx(out, ti, tj)] = s_tstore[threadIdx.x] ? 1 : 0;
+    }
+    // zero fill: stored pixels of active tiles in units without targets
+    if (nun > 1) {
+        const int C = out.C;
+        for (int e = threadIdx.x; e < npx * ((C & 3) == 0 ? C / 4 : C); e += kPlanThreads) {
+            const int per = (C & 3) == 0 ? C / 4 : C;
+            const int p = e / per, q = e - p * per;
+            const int ly = p / BW, lx = p - (p / BW) * BW;
+            if (s_ucnt[(ly / kUY) * upr + lx / kUX] > 0 || !s_tstore[(ly / t) * tpr + lx / t]) continue;
+            const int y = Y0 + ly, x = X0 + lx;
+            if (y < -hs || y >= eh + hs || x < -hs || x >= ew + hs) continue;
+            if ((C & 3) == 0)
+                reinterpret_cast<float4*>(out.d + pkt_off(out, y, x))[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            else
+                out.d[pkt_off(out, y, x) + q] = 0.0f;
+        }
+    }
+}
+
+struct DenseArgs {
+    PktDev in, out;
+    const float* w;  // [nNB][nKB][hi: KC/4 x NBD x 4][lo: same]
+    const int* units;
+    const int* nunits;
+    float* ws;       // split-K partials [S][n*128][cout_pad] (smax > 1)
+    int cin, cout, cout_pad, k, r;
+    int KC, nCB, NBD, nNB, nst;
+    int smax, sms;
+    uint32_t pstr;         // bytes per patch pixel (KC fp32 + 16 B pad: conflict-free row reads)
+    uint32_t patch_bytes;  // one patch buffer
+    uint32_t w_stage;      // bytes of one weight stage (hi + lo)
+    uint32_t acc_cols, nbuf, a_col0;  // TMEM plan
+    int umax;              // units per item the TMEM / smem plan allows (1 or 2)
+    long long* trace;      // microbenchmark (dbg & 64): per-K-block clock64 stamps of CTA 0
+    int dbg;               // microbenchmark knobs (tools/bench_conv.cu): 1 no MMA, 2 no patch, 4 no weights
+};
+
+// Work decomposition for n units x nNB N-blocks x nKB K-blocks, chosen on
+// device from the frame's unit count (the same in every CTA and the reduce):
+// U units per item (2 share each weight stage: half the weight traffic; 1
+// spreads small layers over more SMs) and S K-splits. Cost model in K-block
+// time units: waves x K-blocks per item x (MMA time + ~300 cycles of per-K-block
+// handshake, relative), + a penalty per split for the partials' traffic.
+struct DenseSched {
+    int U, S, items;
+};
+// Work decomposition, chosen on device from the frame's unit count n (the same
+// in every CTA and in the reduce): two units per item (they share each weight
+// stage: half the weight traffic) when there is at least a wave of such items,
+// else one; split-K only when even single-unit items leave most SMs idle
+// (partials cost a workspace round trip).
+__host__ __device__ __forceinline__ DenseSched dense_sched(int n, int nNB, int nKB, int smax, int sms, int umax) {
+    DenseSched d{1, 1, n * nNB};
+    if (umax >= 2 && (long long)((n + 1) / 2) * nNB >= sms) {
+        d.U = 2;
+        d.items = ((n + 1) / 2) * nNB;
+        return d;
+    }
+    while (d.S * 2 <= smax && (long long)n * nNB * d.S * 2 <= sms && nKB / (d.S * 2) >= 4) d.S *= 2;
+    d.items = n * nNB * d.S;
+    return d;
+}
+
+// Warp roles: 0..4*kProdWG-1 A producers, kProdWG warpgroups taking K-blocks
+// round robin (row m = thread; per K-block the pixel's KC hi and lo channels at
+// the tap offset are read from the shared-memory patch and tcgen05.st'ed into
+// the TMEM A stage), then 4 patch loaders (cp.async + TF32 split, one patch per
+// (unit, channel chunk), double buffered), 4 epilogue warps, the MMA issuer and
+// the weight producer.
+constexpr int kProdWG = 3;
+constexpr int kDenseThreads = (4 * kProdWG + 10) * 32;
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]),
+        "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),
+        "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                            uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+// Store KC 32-bit columns of this warp's lane quarter into TMEM.
+template <int KC>
+__device__ __forceinline__ void store_cols(uint32_t taddr, const uint32_t* v) {
+    if constexpr (KC == 32) tmem_st32(taddr, v);
+    else if constexpr (KC == 16) tmem_st16(taddr, v);
+    else tmem_st8(taddr, v);
+}
+
+template <int KC>
+__global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bar_full[8], bar_empty[8], bar_pf[2], bar_pe[2], bar_af[2], bar_ae[2];
+    __shared__ uint32_t tmem_base_sh;
+
+    const FrameDev& F = *c.f;
+    const int n = *a.nunits;
+    const int K2 = a.k * a.k;
+    const int nKB = a.nCB * K2;
+    const DenseSched sch = dense_sched(n, a.nNB, nKB, a.smax, a.sms, a.umax);
+    const int S = sch.S, UPI = sch.U, items = sch.items;
+    if ((int)blockIdx.x >= items) return;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int PW = kUX + 2 * a.r;
+    const int NST = a.nst;
+    // TMEM: accumulators [nbuf][2 units][NBD] then NST A stages of [2 units][hi KC | lo KC]
+    const uint32_t acc_buf = a.umax * a.NBD;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 32) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(smem_u32(&bar_full[i]), 5);  // 4 A-producer warps + the weight bytes
+            mbar_init(smem_u32(&bar_empty[i]), 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&bar_pf[i]), 4);
+            mbar_init(smem_u32(&bar_pe[i]), 4 * kProdWG);
+            mbar_init(smem_u32(&bar_af[i]), 1);
+            mbar_init(smem_u32(&bar_ae[i]), 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+    const uint32_t sbase = smem_u32(smem);
+    if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) a.trace[500] = clock64();
+    // smem: patches [2 buffers][2 units][hi, lo] planes, then the weight stages
+    const uint32_t unit_bytes = 2 * a.patch_bytes, buf_bytes = a.umax * unit_bytes;
+    const uint32_t w_base = sbase + 2 * buf_bytes;
+
+    // item -> (unit pair, N-block, K split) and its K-block range (channel chunk outer, tap inner)
+    auto item_info = [&](int it, int& pr, int& nb, int& kb0, int& kb1) {
+        const int per = a.nNB * S;
+        pr = it / per;
+        const int rem = it - pr * per;
+        nb = rem / S;
+        const int ks = rem - nb * S;
+        kb0 = (int)(((long long)nKB * ks) / S);
+        kb1 = (int)(((long long)nKB * (ks + 1)) / S);
+    };
+
+    if (warp < 4 * kProdWG) {
+        // ------------------------------------------------ A producers (patch rows -> TMEM)
+        // kProdWG warpgroups take K-blocks round robin (tcgen05.st + wait::st is
+        // latency-bound); each writes both units' A rows of its K-block.
+        const int wg = warp >> 2, wq = warp & 3;
+        const int m = tid & 127;  // row = unit pixel (m >> 3, m & 7)
+        const uint32_t row_off = (uint32_t)((m >> 3) * PW + (m & 7)) * a.pstr;
+        uint32_t g = 0, pseq = 0, pst = 0, pph = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            int pr, nb, kb0, kb1;
+            item_info(it, pr, nb, kb0, kb1);
+            const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
+            for (int cb = kb0 / K2; cb <= (kb1 - 1) / K2; ++cb, ++pseq) {
+                const int pb = pseq & 1;
+                mbar_wait(smem_u32(&bar_pf[pb]), (pseq >> 1) & 1);
+                const uint32_t patch = sbase + pb * buf_bytes + row_off;
+                const int t0 = max(kb0 - cb * K2, 0), t1 = min(kb1 - cb * K2, K2);
+                for (int tap = t0; tap < t1; ++tap, ++g) {
+                    const uint32_t st = pst, q = pph;
+                    if (++pst == (uint32_t)NST) pst = 0, pph ^= 1;
+                    if ((int)(g % kProdWG) != wg) continue;
+                    const int ky = tap / a.k, kx = tap - ky * a.k;
+                    const uint32_t src0 = patch + (uint32_t)(ky * PW + kx) * a.pstr;
+                    const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + a.a_col0 + st * 2 * a.umax * KC;
+                    const long long t_a = clock64();
+                    mbar_wait(smem_u32(&bar_empty[st]), q ^ 1);
+                    const long long t_b = clock64();
+                    tc_fence_after();
+                    for (int j = 0; j < nu; ++j) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {  // hi plane, then lo plane
+                            uint32_t v[KC];
+                            const uint32_t src = src0 + j * unit_bytes + h * a.patch_bytes;
+#pragma unroll
+                            for (int q4 = 0; q4 < KC / 4; ++q4)
+                                asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                                             : "=r"(v[4 * q4]), "=r"(v[4 * q4 + 1]), "=r"(v[4 * q4 + 2]),
+                                               "=r"(v[4 * q4 + 3])
+                                             : "r"(src + 16 * q4));
+                            store_cols<KC>(taddr + j * 2 * KC + h * KC, v);
+                        }
+                    }
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(smem_u32(&bar_full[st]));
+                    if ((a.dbg & 64) && blockIdx.x == 0 && tid == 128 * wg && g < 64) {
+                        a.trace[g * 8 + 0] = t_a;
+                        a.trace[g * 8 + 1] = t_b;
+                        a.trace[g * 8 + 2] = clock64();
+                    }
+                }
+                __syncwarp();  // every producer warp is done reading this patch
+                if (lane == 0) mbar_arrive(smem_u32(&bar_pe[pb]));
+            }
+        }
+    } else if (warp < 4 * kProdWG + 4) {
+        // ------------------------------------------------ patch loaders (cp.async, zero fill, TF32 split)
+        const int lt = tid - 128 * kProdWG;
+        const int c4n = KC / 4;
+        const int E1 = PW * (kUY + 2 * a.r) * c4n;
+        const bool vec = (a.in.C & 3) == 0;
+        uint32_t pseq = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            int pr, nb, kb0, kb1;
+            item_info(it, pr, nb, kb0, kb1);
+            const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
+            int y0[2], x0[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int uv = __ldg(a.units + UPI * pr + (j < nu ? j : 0));
+                y0[j] = ((uv >> 16) - 1) * kUY - a.r;
+                x0[j] = ((uv & 0xffff) - 1) * kUX - a.r;
+            }
+            const int E = E1 * nu;
+            for (int cb = kb0 / K2; cb <= (kb1 - 1) / K2; ++cb, ++pseq) {
+                const int pb = pseq & 1;
+                mbar_wait(smem_u32(&bar_pe[pb]), ((pseq >> 1) & 1) ^ 1);
+                const uint32_t buf = sbase + pb * buf_bytes;
+                const int cbase = cb * KC;
+                for (int e = lt; e < E; e += 128) {
+                    const int j = e >= E1 ? 1 : 0;
+                    const int e1 = e - j * E1;
+                    const int p = e1 / c4n, c4 = e1 - p * c4n;
+                    const int py = p / PW, px = p - py * PW;
+                    const int y = (j ? y0[1] : y0[0]) + py, x = (j ? x0[1] : x0[0]) + px;
+                    const int ch = cbase + c4 * 4;
+                    const uint32_t dst = buf + j * unit_bytes + p * a.pstr + c4 * 16;
+                    const bool ok = pkt_ok(a.in, F.th, F.tw, y, x);
+                    if (vec) {
+                        const bool v = ok && ch < a.cin;
+                        cp_async16(dst, v ? a.in.d + pkt_off(a.in, y, x) + ch : a.in.d, v ? 16u : 0u);
+                    } else {
+                        const float* src = ok ? a.in.d + pkt_off(a.in, y, x) : a.in.d;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const bool v = ok && ch + q < a.cin;
+                            cp_async4(dst + 4 * q, v ? src + ch + q : a.in.d, v ? 4u : 0u);
+                        }
+                    }
+                }
+                cp_async_wait_all();
+                // split own elements: hi = x with 13 low mantissa bits cleared (exact TF32),
+                // lo = x - hi (exact; the tensor core reads its top 19 bits)
+                for (int e = lt; e < E; e += 128) {
+                    const int j = e >= E1 ? 1 : 0;
+                    const int e1 = e - j * E1;
+                    const int p = e1 / c4n, c4 = e1 - p * c4n;
+                    const uint32_t hi = buf + j * unit_bytes + p * a.pstr + c4 * 16, lo = hi + a.patch_bytes;
+                    float4 v;
+                    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                                 : "r"(hi));
+                    const uint32_t h0 = __float_as_uint(v.x) & 0xffffe000u, h1 = __float_as_uint(v.y) & 0xffffe000u;
+                    const uint32_t h2 = __float_as_uint(v.z) & 0xffffe000u, h3 = __float_as_uint(v.w) & 0xffffe000u;
+                    const float l0 = __fsub_rn(v.x, __uint_as_float(h0)), l1 = __fsub_rn(v.y, __uint_as_float(h1));
+                    const float l2 = __fsub_rn(v.z, __uint_as_float(h2)), l3 = __fsub_rn(v.w, __uint_as_float(h3));
+                    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(hi), "r"(h0), "r"(h1), "r"(h2), "r"(h3)
+                                 : "memory");
+                    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lo), "f"(l0), "f"(l1), "f"(l2), "f"(l3)
+                                 : "memory");
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bar_pf[pb]));
+            }
+        }
+    } else if (warp < 4 * kProdWG + 8) {
+        // ------------------------------------------------ epilogue: TMEM -> packet / split-K workspace
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const int hs = a.out.halo;
+        const int eh = F.th * a.out.t + hs, ew = F.tw * a.out.t + hs;
+        uint32_t ui = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x, ++ui) {
+            int pr, nb, kb0, kb1;
+            item_info(it, pr, nb, kb0, kb1);
+            const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
+            const uint32_t b = a.nbuf == 2 ? (ui & 1) : 0, ub = a.nbuf == 2 ? (ui >> 1) : ui;
+            mbar_wait(smem_u32(&bar_af[b]), ub & 1);
+            const long long t_e0 = clock64();
+            tc_fence_after();
+            for (int j = 0; j < nu; ++j) {
+                const int u = UPI * pr + j;
+                const int uv = __ldg(a.units + u);
+                const int y = ((uv >> 16) - 1) * kUY + (m >> 3), x = ((uv & 0xffff) - 1) * kUX + (m & 7);
+                const bool valid = y >= -hs && y < eh && x >= -hs && x < ew;  // stored grown extent
+                float* dst_row = nullptr;
+                int lim = a.cout;
+                if (S > 1) {
+                    dst_row = a.ws + ((size_t)((it % S) * n + u) * 128 + m) * a.cout_pad;
+                    lim = a.cout_pad;
+                } else if (valid) {
+                    dst_row = a.out.d + pkt_off(a.out, y, x);
+                }
+                const uint32_t tcol = tmem + b * acc_buf + j * a.NBD + ((uint32_t)(q * 32) << 16);
+                for (int cc = 0; cc < a.NBD; cc += 32) {
+                    float v[32];
+                    tmem_ld32(tcol + (uint32_t)cc, v);
+                    const int o0 = nb * a.NBD + cc;
+                    if (dst_row) {
+                        float* dst = dst_row + o0;
+                        if ((S > 1 || (a.out.C & 3) == 0) && o0 + 32 <= lim) {
+#pragma unroll
+                            for (int k4 = 0; k4 < 8; ++k4)
+                                reinterpret_cast<float4*>(dst)[k4] =
+                                    make_float4(v[4 * k4], v[4 * k4 + 1], v[4 * k4 + 2], v[4 * k4 + 3]);
+                        } else {
+#pragma unroll
+                            for (int k4 = 0; k4 < 32; ++k4)
+                                if (o0 + k4 < lim) dst[k4] = v[k4];
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bar_ae[b]));
+            if ((a.dbg & 64) && blockIdx.x == 0 && tid == 128 * kProdWG + 128 && ui < 4) {
+                a.trace[504 + 2 * ui] = t_e0;
+                a.trace[505 + 2 * ui] = clock64();
+            }
+        }
+    } else if (warp == 4 * kProdWG + 8) {
+        // ------------------------------------------------ MMA issuer
+        // Warp-uniform loop (descriptors in uniform registers); one elected
+        // lane issues the MMAs and commits. Both units use the same weight stage.
+        const uint32_t idesc = idesc_tf32(a.NBD);
+        const uint32_t lbo_b = (uint32_t)a.NBD * 16, half_w = a.w_stage / 2;
+        uint32_t st = 0, ph = 0, ui = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x, ++ui) {
+            int pr, nb, kb0, kb1;
+            item_info(it, pr, nb, kb0, kb1);
+            const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
+            const uint32_t b = a.nbuf == 2 ? (ui & 1) : 0, ub = a.nbuf == 2 ? (ui >> 1) : ui;
+            mbar_wait(smem_u32(&bar_ae[b]), (ub & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t dtm = tmem + b * acc_buf;
+            // two K-blocks per handshake: wait for both stages, issue both MMA
+            // chains back to back (the per-K-block wait/fence overhead is
+            // otherwise a bubble in the tensor pipe)
+            for (int kb = kb0; kb < kb1; kb += 2) {
+                const bool two = kb + 1 < kb1;
+                const uint32_t st1 = st + 1 == (uint32_t)NST ? 0 : st + 1;
+                const uint32_t ph1 = st + 1 == (uint32_t)NST ? ph ^ 1 : ph;
+                mbar_wait(smem_u32(&bar_full[st]), ph);
+                if (two) mbar_wait(smem_u32(&bar_full[st1]), ph1);
+                tc_fence_after();
+                if (elect_one()) {
+#pragma unroll 1
+                    for (int h = 0; h < (two ? 2 : 1); ++h) {
+                        const uint32_t sh = h ? st1 : st;
+                        const uint32_t wb = w_base + sh * a.w_stage;
+                        const uint32_t a_tm = tmem + a.a_col0 + sh * 2 * a.umax * KC;
+                        if (!(a.dbg & 1)) {
+#pragma unroll
+                            for (int j = 0; j < KC / 8; ++j) {
+                                const uint64_t dbh = umma_desc(wb + 2 * j * lbo_b, lbo_b, 128);
+                                const uint64_t dbl = umma_desc(wb + half_w + 2 * j * lbo_b, lbo_b, 128);
+                                const uint32_t acc = (kb + h > kb0 || j > 0) ? 1u : 0u;
+                                for (int uu = 0; uu < nu; ++uu) {
+                                    const uint32_t d = dtm + uu * a.NBD, at = a_tm + uu * 2 * KC;
+                                    mma_tf32_ts(d, at + KC + 8 * j, dbh, idesc, acc);
+                                    mma_tf32_ts(d, at + 8 * j, dbl, idesc, 1u);
+                                    mma_tf32_ts(d, at + 8 * j, dbh, idesc, 1u);
+                                }
+                            }
+                        }
+                        mma_commit(smem_u32(&bar_empty[sh]));
+                    }
+                }
+                __syncwarp();
+                if (two) {
+                    st = st1 + 1 == (uint32_t)NST ? 0 : st1 + 1;
+                    ph = st1 + 1 == (uint32_t)NST ? ph1 ^ 1 : ph1;
+                } else {
+                    st = st1, ph = ph1;
+                }
+            }
+            if (elect_one()) mma_commit(smem_u32(&bar_af[b]));
+            __syncwarp();
+        }
+    } else {
+        // ------------------------------------------------ weight producer
+        if (lane == 0) {
+            uint32_t st = 0, ph = 0;
+            for (int it = blockIdx.x; it < items; it += gridDim.x) {
+                int pr, nb, kb0, kb1;
+                item_info(it, pr, nb, kb0, kb1);
+                const float* wnb = a.w + (size_t)nb * nKB * (a.w_stage / 4);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(smem_u32(&bar_empty[st]), ph ^ 1);
+                    if (a.dbg & 4) {
+                        mbar_arrive(smem_u32(&bar_full[st]));
+                    } else {
+                        mbar_arrive_tx(smem_u32(&bar_full[st]), a.w_stage);
+                        bulk_g2s(w_base + st * a.w_stage, wnb + (size_t)kb * (a.w_stage / 4), a.w_stage,
+                                 smem_u32(&bar_full[st]));
+                    }
+                    if (++st == (uint32_t)NST) st = 0, ph ^= 1;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if ((a.dbg & 64) && blockIdx.x == 0 && lane == 0 && warp < 32) a.trace[520 + warp] = clock64();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) a.trace[501] = clock64();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// Fixed-order split-K reduction of the dense partials into the packet.
+__global__ void k_conv_dense_reduce(Ctx c, DenseArgs a) {
+    const FrameDev& F = *c.f;
+    const int n = *a.nunits;
+    const int S = dense_sched(n, a.nNB, a.nCB * a.k * a.k, a.smax, a.sms, a.umax).S;
+    if (S <= 1) return;
+    const int hs = a.out.halo;
+    const int eh = F.th * a.out.t + hs, ew = F.tw * a.out.t + hs;
+    const long long total = (long long)n * 128 * a.cout;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long row = e / a.cout;
+        const int o = (int)(e - row * a.cout);
+        const int u = (int)(row >> 7), m = (int)(row & 127);
+        const int uv = __ldg(a.units + u);
+        const int y = ((uv >> 16) - 1) * kUY + (m >> 3), x = ((uv & 0xffff) - 1) * kUX + (m & 7);
+        if (y < -hs || y >= eh || x < -hs || x >= ew) continue;
+        float sum = a.ws[(size_t)row * a.cout_pad + o];
+        for (int sp = 1; sp < S; ++sp) sum = __fadd_rn(sum, a.ws[((size_t)sp * n * 128 + row) * a.cout_pad + o]);
+        a.out.d[pkt_off(a.out, y, x) + o] = sum;
+    }
+}
+
+uint32_t rna_tf32_bits(float x) {
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u) return u;
+    return (u + 0x1000u) & 0xffffe000u;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host side
+DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int cols, size_t ws_budget_bytes) {
+    DenseConvPlan p{};
+    p.cin_pad = (cin + 7) / 8 * 8;
+    p.cout_pad = (cout + 31) / 32 * 32;
+    p.NBD = p.cout_pad < 128 ? p.cout_pad : 128;
+    if (p.cout_pad % p.NBD) p.NBD = 32;
+    p.nNB = p.cout_pad / p.NBD;
+    // One unit per item (measured best on the C2 layers: more SMs busy, and
+    // 32-channel K-blocks amortise the per-K-block handshake); the kernel also
+    // supports two units sharing each weight stage (umax = 2).
+    p.umax = 1;
+    p.KC = p.cin_pad % 32 == 0 ? 32 : (p.cin_pad % 16 == 0 ? 16 : 8);
+    p.nCB = p.cin_pad / p.KC;
+    p.r = k / 2;
+    p.k = k;
+    const int PW = kUX + 2 * p.r, PH = kUY + 2 * p.r;
+    p.s_c4 = (unsigned)p.KC * 4 + 16;  // pixel stride in a patch plane (conflict-free row reads)
+    p.patch_bytes = ((unsigned)PW * PH * p.s_c4 + 127) / 128 * 128;
+    p.w_stage = (uint32_t)p.NBD * p.KC * 8;
+    const unsigned acc = (unsigned)p.umax * p.NBD;
+    const size_t budget = 200 * 1024;
+    auto fits = [&](int nst, unsigned nbuf) {
+        return 4 * (size_t)p.umax * p.patch_bytes + (size_t)nst * p.w_stage <= budget &&
+               nbuf * acc + (unsigned)nst * 2 * p.umax * p.KC <= 512;
+    };
+    // prefer double-buffered accumulators with >= 4 stages, else single with more stages
+    p.nbuf = 2;
+    p.nstw = 8;
+    while (p.nstw > 4 && !fits(p.nstw, 2)) --p.nstw;
+    if (!fits(p.nstw, 2)) {
+        p.nbuf = 1;
+        p.nstw = 8;
+        while (p.nstw > 2 && !fits(p.nstw, 1)) --p.nstw;
+    }
+    p.acc_cols = acc;
+    p.smem = 4 * (size_t)p.umax * p.patch_bytes + (size_t)p.nstw * p.w_stage;
+    const int BH = t_out > kUY ? t_out : kUY, BW = t_out > kUX ? t_out : kUX;
+    p.ok = fits(p.nstw, p.nbuf) && k * k <= 49 && (k & 1) && t_out <= 64 && (BH / kUY) * (BW / kUX) <= 32 &&
+           (BH / t_out) * (BW / t_out) <= 32;
+    // units over [-16, rows*t + hg) x [-8, cols*t + hg) (hg <= 8 px of grown halo)
+    p.nux_max = (cols * t_out + 8 + kUX - 1) / kUX + 1;
+    p.nuy_max = (rows * t_out + 8 + kUY - 1) / kUY + 1;
+    p.units_max = p.nux_max * p.nuy_max;
+    p.nbh = (rows * t_out + 8 + BH - 1) / BH + 1;
+    p.nbw = (cols * t_out + 8 + BW - 1) / BW + 1;
+    p.t_out = t_out;
+    p.smax = 8;
+    while (p.smax > 1 && (size_t)p.smax * p.units_max * 128 * p.cout_pad * 4 > ws_budget_bytes) p.smax /= 2;
+    return p;
+}
+
+size_t dense_conv_weight_floats(const DenseConvPlan& p) {
+    return (size_t)p.nNB * p.nCB * p.k * p.k * p.NBD * p.KC * 2;
+}
+
+void dense_conv_prepare_weights(const DenseConvPlan& p, const float* w, int cin, int cout, float* outp) {
+    const int K2 = p.k * p.k, nKB = p.nCB * K2;
+    memset(outp, 0, dense_conv_weight_floats(p) * sizeof(float));
+    const size_t blob = (size_t)p.NBD * p.KC * 2;
+    for (int nb = 0; nb < p.nNB; ++nb)
+        for (int kb = 0; kb < nKB; ++kb) {
+            const int cb = kb / K2, tap = kb % K2;
+            float* b = outp + ((size_t)nb * nKB + kb) * blob;
+            for (int nn = 0; nn < p.NBD; ++nn) {
+                const int o = nb * p.NBD + nn;
+                for (int ci = 0; ci < p.KC; ++ci) {
+                    const int i = cb * p.KC + ci;
+                    float x = 0.0f;
+                    if (o < cout && i < cin) x = w[((size_t)o * cin + i) * K2 + tap];
+                    const uint32_t hb = rna_tf32_bits(x);
+                    float hi;
+                    memcpy(&hi, &hb, 4);
+                    const uint32_t lb = rna_tf32_bits(x - hi);
+                    float lo;
+                    memcpy(&lo, &lb, 4);
+                    const size_t off = ((size_t)(ci / 4) * p.NBD + nn) * 4 + (ci % 4);
+                    b[off] = hi;
+                    b[(size_t)p.NBD * p.KC + off] = lo;
+                }
+            }
+        }
+}
+
+void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, int hg, int* units,
+                      int* nunits, unsigned long long* flop_px) {
+    if (hg > 8) throw std::runtime_error("conv_plan: grown halo > 8 px");
+    k_conv_plan<<<p.nbh * p.nbw, kPlanThreads, 0, s>>>(c, in, out, p.k, p.r, hg, p.nbw, units, nunits, flop_px);
+}
+
+template <int KC>
+static void launch_kc(int grid, size_t smem, cudaStream_t s, const Ctx& c, const DenseArgs& a) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_conv_dense<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = true;
+    }
+    k_conv_dense<KC><<<grid, kDenseThreads, smem, s>>>(c, a);
+}
+
+static long long* g_trace = nullptr;
+long long* dense_conv_trace_buffer() { return g_trace; }
+void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,
+                       int cin, int cout, const int* units, const int* nunits, float* ws, int num_sms) {
+    if (!p.ok) throw std::runtime_error("conv_dense: unsupported layer shape");
+    DenseArgs a{in, out, w, units, nunits, p.smax > 1 ? ws : nullptr, cin, cout, p.cout_pad, p.k, p.r,
+                p.KC, p.nCB, p.NBD, p.nNB, p.nstw, p.smax > 1 ? p.smax : 1, num_sms, p.s_c4, p.patch_bytes,
+                p.w_stage, p.acc_cols, p.nbuf, p.nbuf * p.acc_cols, p.umax, nullptr, 0};
+    if (getenv("DFX_CONV_DBG") && !g_trace) cudaMalloc(&g_trace, 1024 * 8);
+    a.trace = g_trace;
+    if (const char* d = getenv("DFX_CONV_DBG")) a.dbg = atoi(d);
+    DenseConvPlan pp = p;
+    if (a.dbg & 128) a.smax = 1;  // microbenchmark: no split-K
+    if (const char* d = getenv("DFX_CONV_NST")) {  // microbenchmark: fewer pipeline stages
+        const int v = atoi(d);
+        if (v >= 2 && v < pp.nstw) a.nst = v;
+    }
+    const long long max_items = (long long)p.units_max * p.nNB * a.smax;
+    const int grid = (int)(max_items < num_sms ? (max_items < 1 ? 1 : max_items) : num_sms);
+    if (p.KC == 32) launch_kc<32>(grid, p.smem, s, c, a);
+    else if (p.KC == 16) launch_kc<16>(grid, p.smem, s, c, a);
+    else launch_kc<8>(grid, p.smem, s, c, a);
+    if (a.smax > 1) k_conv_dense_reduce<<<num_sms * 4, 256, 0, s>>>(c, a);
+}
+
+}  // namespace dfx

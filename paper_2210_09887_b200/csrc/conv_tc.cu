@@ -8,7 +8,7 @@
 // partial tiles, ring pixels), N = Cout (<= 256 per MMA), K = k*k*Cin walked
 // as K-blocks of (tap, 32 input channels).
 //
-// Arithmetic: 3xTF32 (x = hi + lo with hi = rna_tf32(x), lo = rna_tf32(x - hi);
+// Arithmetic: 3xTF32 (x = hi + lo with hi = x truncated to TF32, lo = x - hi;
 // D += Ahi*Bhi + Ahi*Blo + Alo*Bhi, fp32 accumulate in TMEM) — fp32-grade
 // accuracy (|err| ~1e-6 relative), within the stated 1e-4 tolerance of the
 // reference's fp32 outputs.
@@ -116,6 +116,11 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
         "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),
         "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
         : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -315,11 +320,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1) k_conv_tc(Ctx c, ConvArgs a) {
             {
                 uint32_t part[kKC];
                 const uint32_t taddr = tmem + ((uint32_t)(wid_in_wg * 32) << 16) + a_col0 + st * 64;
+                // hi = x with the 13 low mantissa bits cleared (exact TF32); lo = x - hi is
+                // exact in fp32 and the tensor core reads its top 19 bits.
 #pragma unroll
-                for (int j = 0; j < kKC; ++j) part[j] = to_tf32(cur[j]);
+                for (int j = 0; j < kKC; ++j) part[j] = __float_as_uint(cur[j]) & 0xffffe000u;
                 tmem_st32(taddr, part);
 #pragma unroll
-                for (int j = 0; j < kKC; ++j) part[j] = to_tf32(__fsub_rn(cur[j], __uint_as_float(to_tf32(cur[j]))));
+                for (int j = 0; j < kKC; ++j)
+                    part[j] = __float_as_uint(__fsub_rn(cur[j], __uint_as_float(__float_as_uint(cur[j]) & 0xffffe000u)));
                 tmem_st32(taddr + 32, part);
             }
             tmem_wait_st();
@@ -378,27 +386,28 @@ __global__ void __launch_bounds__(kThreadsV2, 1) k_conv_tc(Ctx c, ConvArgs a) {
             if (lane == 0) mbar_arrive(smem_u32(&bar_acce[b]));
         }
     } else {
-        // ------------------------------------------------ MMA issuer (one thread)
-        if (lane == 0) {
-            uint32_t g = 0, ui = 0;
-            for (int u = blockIdx.x; u < units; u += gridDim.x, ++ui) {
-                int mb, nb, kb0, kb1;
-                unit_info(u, mb, nb, kb0, kb1);
-                const int NB = (a.cout_pad - nb * 256) < 256 ? (a.cout_pad - nb * 256) : 256;
-                const uint32_t idesc = idesc_tf32(NB);
-                const uint32_t lbo_b = (uint32_t)NB * 16;
-                const uint32_t b = nbuf == 2 ? (ui & 1) : 0, ub = nbuf == 2 ? (ui >> 1) : ui;
-                mbar_wait(smem_u32(&bar_acce[b]), (ub & 1) ^ 1);
+        // ------------------------------------------------ MMA issuer
+        // Warp-uniform loop (descriptors in uniform registers); one elected
+        // lane issues the MMAs and commits.
+        uint32_t st = 0, ph = 0, ui = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++ui) {
+            int mb, nb, kb0, kb1;
+            unit_info(u, mb, nb, kb0, kb1);
+            const int NB = (a.cout_pad - nb * 256) < 256 ? (a.cout_pad - nb * 256) : 256;
+            const uint32_t idesc = idesc_tf32(NB);
+            const uint32_t lbo_b = (uint32_t)NB * 16;
+            const uint32_t b = nbuf == 2 ? (ui & 1) : 0, ub = nbuf == 2 ? (ui >> 1) : ui;
+            mbar_wait(smem_u32(&bar_acce[b]), (ub & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t dtm = tmem + b * acc_cols;
+            for (int kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(smem_u32(&bar_full[st]), ph);
                 tc_fence_after();
-                const uint32_t dtm = tmem + b * acc_cols;
-                for (int kb = kb0; kb < kb1; ++kb, ++g) {
-                    const uint32_t st = g % NST, q = g / NST;
-                    mbar_wait(smem_u32(&bar_full[st]), q & 1);
-                    tc_fence_after();
-                    const int c0 = (kb / K2) * kKC;
-                    const int nsteps = (a.cin_pad - c0) / 8 < 4 ? (a.cin_pad - c0) / 8 : 4;
-                    const uint32_t b_base = smem_base + st * stage_bytes;
-                    const uint32_t a_tm = tmem + a_col0 + st * 64;
+                const int c0 = (kb / K2) * kKC;
+                const int nsteps = (a.cin_pad - c0) / 8 < 4 ? (a.cin_pad - c0) / 8 : 4;
+                const uint32_t b_base = smem_base + st * stage_bytes;
+                const uint32_t a_tm = tmem + a_col0 + st * 64;
+                if (elect_one()) {
                     for (int j = 0; j < nsteps; ++j) {
                         const uint64_t dbh = umma_desc(b_base + 2 * j * lbo_b, lbo_b, 128);
                         const uint64_t dbl = umma_desc(b_base + (uint32_t)NB * kKC * 4 + 2 * j * lbo_b, lbo_b, 128);
@@ -408,10 +417,12 @@ __global__ void __launch_bounds__(kThreadsV2, 1) k_conv_tc(Ctx c, ConvArgs a) {
                     }
                     mma_commit(smem_u32(&bar_empty[st]));
                 }
-                mma_commit(smem_u32(&bar_accf[b]));
+                __syncwarp();
+                if (++st == (uint32_t)NST) st = 0, ph ^= 1;
             }
+            if (elect_one()) mma_commit(smem_u32(&bar_accf[b]));
+            __syncwarp();
         }
-        __syncwarp();
     }
     tc_fence_before();
     __syncthreads();

@@ -9,6 +9,7 @@
 // on one CUDA stream. Every per-frame value the kernels need is read on device
 // from the uploaded FrameDev block, so the launch sequence is shape-stable.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -172,6 +173,11 @@ class Engine {
         int max_targets = 0;
         int splits = 1;
         DevArr<float> ws;
+        // dense-unit path (conv_dense.cu)
+        bool dense = false;
+        DenseConvPlan dp{};
+        DevArr<float> wdense, wsd;
+        DevArr<int> units;
     };
 
     void allocate(int th, int tw);
@@ -219,7 +225,7 @@ class Engine {
     int nclaim_bufs_ = 0;
     // per-frame counters: [nl u64 flop_px][u64 dropped][nl int counts][nl * slots u32 tile_max]
     DevArr<uint8_t> counters_d_;
-    size_t cnt_bytes_ = 0, off_dropped_ = 0, off_counts_ = 0, off_tmax_ = 0;
+    size_t cnt_bytes_ = 0, off_dropped_ = 0, off_counts_ = 0, off_ucounts_ = 0, off_tmax_ = 0;
     uint8_t* readback_h_ = nullptr;  // pinned: flop_px, dropped, input mask
     // output
     DevArr<float> out_d_;
@@ -360,6 +366,19 @@ void Engine::allocate(int th, int tw) {
                     CUDA_CHECK(cudaMemcpy(rt.wtc.p, ws.data(), ws.size() * 4, cudaMemcpyHostToDevice));
                     rt.splits = conv_tc_splits(rt.max_targets, rt.cin_pad, rt.cout_pad, l.k, num_sms_);
                     if (rt.splits > 1) rt.ws.alloc((size_t)rt.splits * rt.max_targets * rt.cout_pad);
+                    const char* dv = getenv("DFX_DENSE");
+                    if (l.stride == 1 && !(dv && dv[0] == '0')) {
+                        rt.dp = dense_conv_plan(l.cin, l.cout, l.k, l.tile, rows_, cols_, (size_t)256 << 20);
+                        rt.dense = rt.dp.ok;
+                    }
+                    if (rt.dense) {
+                        std::vector<float> wd(dense_conv_weight_floats(rt.dp));
+                        dense_conv_prepare_weights(rt.dp, l.w.data(), l.cin, l.cout, wd.data());
+                        rt.wdense.alloc(wd.size());
+                        CUDA_CHECK(cudaMemcpy(rt.wdense.p, wd.data(), wd.size() * 4, cudaMemcpyHostToDevice));
+                        rt.units.alloc(rt.dp.units_max);
+                        if (rt.dp.smax > 1) rt.wsd.alloc((size_t)rt.dp.smax * rt.dp.units_max * 128 * rt.dp.cout_pad);
+                    }
                 }
                 break;
             }
@@ -453,7 +472,8 @@ void Engine::allocate(int th, int tw) {
     const size_t nl = net_.layers.size();
     off_dropped_ = nl * 8;
     off_counts_ = off_dropped_ + 8;
-    off_tmax_ = (off_counts_ + nl * 4 + 15) / 16 * 16;
+    off_ucounts_ = off_counts_ + nl * 4;
+    off_tmax_ = (off_ucounts_ + nl * 4 + 15) / 16 * 16;
     cnt_bytes_ = off_tmax_ + nl * (size_t)slots * 4;
     counters_d_.alloc(cnt_bytes_);
     CUDA_CHECK(cudaMallocHost(&readback_h_, nl * 8 + 8 + slots));
@@ -600,6 +620,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     auto* flop_px = reinterpret_cast<unsigned long long*>(counters_d_.p);
     auto* dropped = reinterpret_cast<unsigned long long*>(counters_d_.p + off_dropped_);
     int* counts = reinterpret_cast<int*>(counters_d_.p + off_counts_);
+    int* ucounts = reinterpret_cast<int*>(counters_d_.p + off_ucounts_);
     unsigned* tmax = reinterpret_cast<unsigned*>(counters_d_.p + off_tmax_);
     const int nslots = rows_ * cols_;
 
@@ -636,6 +657,15 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
         const PktDev a = in_packet(l.in0);
         switch (l.kind) {
             case DFX_CONV:
+                if (rt.dense) {
+                    // every target of a stride-1 conv is computed by dense units
+                    PROF(DFX_FAM_CONV_TARGETS, launch_conv_plan(C, s, rt.dp, a, rt.pkt, rt.halo_geom, rt.units.p,
+                                                                ucounts + idx2, flop_px + idx2));
+                    PROF(DFX_FAM_CONV_MMA, launch_conv_dense(C, s, rt.dp, a, rt.pkt, rt.wdense.p, l.cin, l.cout,
+                                                             rt.units.p, ucounts + idx2, rt.wsd.p, num_sms_));
+                    if (rt.dp.smax > 1) ++launches_;
+                    break;
+                }
                 PROF(DFX_FAM_CONV_TARGETS, launch_conv_targets(C, s, a, l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom, rt.list.p, counts + idx2,
                                     flop_px + idx2));
                 {

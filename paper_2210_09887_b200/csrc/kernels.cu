@@ -664,7 +664,8 @@ __device__ __forceinline__ void tile_px_range(const FrameDev& F, const PktDev& o
 constexpr int kTgtMaxPx = 4096;  // t_out <= 64
 __global__ void __launch_bounds__(256) k_conv_targets(Ctx c, PktDev in, int k, int s, int r, PktDev out, int hg,
                                                       int* __restrict__ list, int* __restrict__ count,
-                                                      unsigned long long* __restrict__ flop_px) {
+                                                      unsigned long long* __restrict__ flop_px,
+                                                      const uint8_t* __restrict__ dense_map, int nux_max) {
     __shared__ uint32_t s_bits[kTgtMaxPx / 32];
     __shared__ uint8_t s_nb[8][8];
     __shared__ int s_tr0, s_tc0;
@@ -737,6 +738,11 @@ __global__ void __launch_bounds__(256) k_conv_targets(Ctx c, PktDev in, int k, i
         return (s_bits[p >> 5] >> (p & 31)) & 1u;
     };
     const int sw = x1 - x0, sn = (y1 - y0) * sw;
+    // pixels of dense units are written whole by k_conv_dense
+    const int exh = F.th * t, exw = F.tw * t;
+    auto dense = [&](int oy, int ox) {
+        return dense_map && oy >= 0 && oy < exh && ox >= 0 && ox < exw && dense_map[(oy >> 4) * nux_max + (ox >> 3)];
+    };
     // list append: one atomic per warp
     for (int p0 = 0; p0 < sn; p0 += blockDim.x) {
         const int p = p0 + threadIdx.x;
@@ -745,7 +751,7 @@ __global__ void __launch_bounds__(256) k_conv_targets(Ctx c, PktDev in, int k, i
         if (p < sn) {
             oy = y0 + p / sw;
             ox = x0 + p % sw;
-            tgt = bit(oy, ox);
+            tgt = bit(oy, ox) && !dense(oy, ox);
         }
         const unsigned m = __ballot_sync(0xffffffffu, tgt);
         int base = 0;
@@ -760,13 +766,14 @@ __global__ void __launch_bounds__(256) k_conv_targets(Ctx c, PktDev in, int k, i
         for (int e = threadIdx.x; e < sn * c4; e += blockDim.x) {
             const int p = e / c4, q = e - p * c4;
             const int oy = y0 + p / sw, ox = x0 + p % sw;
-            if (!bit(oy, ox)) reinterpret_cast<float4*>(out.d + pkt_off(out, oy, ox))[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (!bit(oy, ox) && !dense(oy, ox))
+                reinterpret_cast<float4*>(out.d + pkt_off(out, oy, ox))[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
     } else {
         for (int e = threadIdx.x; e < sn * C; e += blockDim.x) {
             const int p = e / C, q = e - p * C;
             const int oy = y0 + p / sw, ox = x0 + p % sw;
-            if (!bit(oy, ox)) out.d[pkt_off(out, oy, ox) + q] = 0.0f;
+            if (!bit(oy, ox) && !dense(oy, ox)) out.d[pkt_off(out, oy, ox) + q] = 0.0f;
         }
     }
 }
@@ -1165,10 +1172,10 @@ void launch_add(const Ctx& c, cudaStream_t s, PktDev a, PktDev b, PktDev out) {
     k_add<<<ext_blocks(c, out), kThreads, 0, s>>>(c, a, b, out);
 }
 void launch_conv_targets(const Ctx& c, cudaStream_t s, PktDev in, int k, int st, int r, PktDev out, int hg, int* list,
-                         int* count, unsigned long long* flop_px) {
+                         int* count, unsigned long long* flop_px, const uint8_t* dense_map, int nux_max) {
     const int RTg = (hg + out.t - 1) / out.t;
     k_conv_targets<<<(c.rows + 2 * RTg) * (c.cols + 2 * RTg), kThreads, 0, s>>>(c, in, k, st, r, out, hg, list, count,
-                                                                                flop_px);
+                                                                                flop_px, dense_map, nux_max);
 }
 void launch_conv_exact(const Ctx& c, cudaStream_t s, PktDev in, const float* w, int cin, int cout, int k, int st, int r,
                        PktDev out, int hg, const int* list, const int* count, int max_targets) {

@@ -67,8 +67,11 @@ void launch_add(const Ctx& c, cudaStream_t s, PktDev a, PktDev b, PktDev out);
 // H = geometric out halo), count (targets in the stored extent) and flops
 // counter (targets in the geometric grown extent), the out ext map, and
 // zeros every non-target pixel of every active out tile.
+// dense_map (nullable): per 16x8 output unit, 1 = computed by k_conv_dense;
+// its pixels are left out of the gathered list and of the zero fill.
 void launch_conv_targets(const Ctx& c, cudaStream_t s, PktDev in, int k, int st, int r, PktDev out,
-                         int out_halo_geom, int* list, int* count, unsigned long long* flop_px);
+                         int out_halo_geom, int* list, int* count, unsigned long long* flop_px,
+                         const uint8_t* dense_map = nullptr, int nux_max = 0);
 void launch_conv_exact(const Ctx& c, cudaStream_t s, PktDev in, const float* w, int cin, int cout, int k, int st,
                        int r, PktDev out, int out_halo_geom, const int* list, const int* count, int max_targets);
 // tcgen05 3xTF32 conv (conv_tc.cu). wsplit: pre-split weights, see conv_tc.cu.
@@ -80,6 +83,26 @@ void launch_conv_tc(const Ctx& c, cudaStream_t s, PktDev in, const float* wsplit
 int conv_tc_splits(int max_targets, int cin_pad, int cout_pad, int k, int num_sms);
 size_t conv_tc_weight_floats(int cin_pad, int cout_pad, int k);
 void conv_tc_prepare_weights(const float* w, int cin, int cout, int k, int cin_pad, int cout_pad, float* out);
+
+// Dense-unit conv (conv_dense.cu): stride-1 convs, 16x8-pixel output units
+// whose pixels are mostly targets; input patches staged once in shared memory.
+struct DenseConvPlan {
+    bool ok;
+    int k, r, cin_pad, KC, nCB, cout_pad, NBD, nNB, nstw, smax, umax;
+    int nux_max, nuy_max, units_max, nbh, nbw, t_out;
+    unsigned s_c4, patch_bytes, w_stage, acc_cols, nbuf;
+    size_t smem;
+};
+DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int cols, size_t ws_budget_bytes);
+size_t dense_conv_weight_floats(const DenseConvPlan& p);
+void dense_conv_prepare_weights(const DenseConvPlan& p, const float* w, int cin, int cout, float* out);
+// Targets, exact out ext map, FLOP pixels, dense unit list and zero fill of a
+// stride-1 conv whose every target is computed by k_conv_dense.
+void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, int hg, int* units,
+                      int* nunits, unsigned long long* flop_px);
+long long* dense_conv_trace_buffer();  // microbenchmark stamps (DFX_CONV_DBG & 64)
+void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,
+                       int cin, int cout, const int* units, const int* nunits, float* ws, int num_sms);
 
 // ---- output (delta_layers.cpp:395-400) ----
 void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out);
