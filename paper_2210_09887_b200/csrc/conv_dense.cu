@@ -40,6 +40,7 @@
 #include <stdexcept>
 
 #include "kernels.hpp"
+#include "pdl.hpp"
 
 namespace dfx {
 
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
                                                             int nbw, int* __restrict__ units,
                                                             int* __restrict__ nunits,
                                                             unsigned long long* __restrict__ flop_px) {
+    pdl_enter();
     __shared__ uint32_t s_bits[4096 / 32];
     __shared__ int s_ucnt[32];
     __shared__ int s_tstore[32];
@@ -328,6 +330,7 @@ __device__ __forceinline__ void store_cols(uint32_t taddr, const uint32_t* v) {
 
 template <int KC>
 __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArgs a) {
+    pdl_enter();
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar_full[8], bar_empty[8], bar_pf[2], bar_pe[2], bar_af[2], bar_ae[2];
     __shared__ uint32_t tmem_base_sh;
@@ -659,6 +662,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
 
 // Fixed-order split-K reduction of the dense partials into the packet.
 __global__ void k_conv_dense_reduce(Ctx c, DenseArgs a) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int n = *a.nunits;
     const int S = dense_sched(n, a.nNB, a.nCB * a.k * a.k, a.smax, a.sms, a.umax).S;
@@ -776,7 +780,7 @@ void dense_conv_prepare_weights(const DenseConvPlan& p, const float* w, int cin,
 void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, int hg, int* units,
                       int* nunits, unsigned long long* flop_px) {
     if (hg > 8) throw std::runtime_error("conv_plan: grown halo > 8 px");
-    k_conv_plan<<<p.nbh * p.nbw, kPlanThreads, 0, s>>>(c, in, out, p.k, p.r, hg, p.nbw, units, nunits, flop_px);
+    launch_pdl(k_conv_plan, p.nbh * p.nbw, kPlanThreads, 0, s, c, in, out, p.k, p.r, hg, p.nbw, units, nunits, flop_px);
 }
 
 template <int KC>
@@ -786,7 +790,7 @@ static void launch_kc(int grid, size_t smem, cudaStream_t s, const Ctx& c, const
         cudaFuncSetAttribute(k_conv_dense<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         configured = true;
     }
-    k_conv_dense<KC><<<grid, kDenseThreads, smem, s>>>(c, a);
+    launch_pdl(k_conv_dense<KC>, grid, kDenseThreads, smem, s, c, a);
 }
 
 static long long* g_trace = nullptr;
@@ -811,7 +815,7 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
     if (p.KC == 32) launch_kc<32>(grid, p.smem, s, c, a);
     else if (p.KC == 16) launch_kc<16>(grid, p.smem, s, c, a);
     else launch_kc<8>(grid, p.smem, s, c, a);
-    if (a.smax > 1) k_conv_dense_reduce<<<num_sms * 4, 256, 0, s>>>(c, a);
+    if (a.smax > 1) launch_pdl(k_conv_dense_reduce, num_sms * 4, 256, 0, s, c, a);
 }
 
 }  // namespace dfx

@@ -34,6 +34,7 @@
 #include <string>
 
 #include "kernels.hpp"
+#include "pdl.hpp"
 
 namespace dfx {
 
@@ -181,6 +182,7 @@ struct ConvArgs {
 
 template <int NST>
 __global__ void __launch_bounds__(kThreadsV2, 1) k_conv_tc(Ctx c, ConvArgs a) {
+    pdl_enter();
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar_full[NST], bar_empty[NST], bar_accf[2], bar_acce[2];
     __shared__ uint32_t tmem_base_sh;
@@ -433,6 +435,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) k_conv_tc(Ctx c, ConvArgs a) {
 
 // Fixed-order split-K reduction into the output packet (deterministic).
 __global__ void k_conv_splitk_reduce(ConvArgs a) {
+    pdl_enter();
     const int n = *a.count;
     const long long total = (long long)n * a.cout;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -509,7 +512,7 @@ static void launch_nst(int grid, size_t smem, cudaStream_t s, const Ctx& c, cons
         cudaFuncSetAttribute(k_conv_tc<NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         configured = true;
     }
-    k_conv_tc<NST><<<grid, kThreadsV2, smem, s>>>(c, a);
+    launch_pdl(k_conv_tc<NST>, grid, kThreadsV2, smem, s, c, a);
 }
 
 void launch_conv_tc(const Ctx& c, cudaStream_t s, PktDev in, const float* wsplit, int cin, int cin_pad, int cout,
@@ -541,7 +544,7 @@ void launch_conv_tc(const Ctx& c, cudaStream_t s, PktDev in, const float* wsplit
         long long total = (long long)max_targets * cout;
         int rg = (int)((total + 255) / 256);
         if (rg > num_sms * 8) rg = num_sms * 8;
-        k_conv_splitk_reduce<<<rg < 1 ? 1 : rg, 256, 0, s>>>(a);
+        launch_pdl(k_conv_splitk_reduce, rg < 1 ? 1 : rg, 256, 0, s, a);
     }
 }
 

@@ -186,7 +186,7 @@ class Engine {
     void finish_info(dfx_frame_info* info);
     void ensure_staging(int c, int h, int w, bool host_frame);
     PktDev in_packet(int idx) const { return idx == -1 ? in_pkt_ : lrt_[idx].pkt; }
-    Ctx ctx() const { return Ctx{d_frame_, d_slots_, rows_, cols_}; }
+    Ctx ctx() const { return Ctx{d_frame_, d_slots_, rows_, cols_, d_own_}; }
 
     Net net_;
     dfx_engine_config cfg_;
@@ -214,11 +214,12 @@ class Engine {
     uint8_t* params_hb_[2] = {nullptr, nullptr};
     cudaEvent_t params_ev_[2] = {nullptr, nullptr};
     int pslot_ = 0;
-    size_t params_bytes_ = 0, off_slots_ = 0, off_claims_ = 0, off_fresh_ = 0;
+    size_t params_bytes_ = 0, off_slots_ = 0, off_claims_ = 0, off_fresh_ = 0, off_own_ = 0;
     FrameDev* d_frame_ = nullptr;
     SlotDev* d_slots_ = nullptr;
     int* d_claims_ = nullptr;
     uint8_t* d_fresh_ = nullptr;
+    uint8_t* d_own_ = nullptr;
     int max_claims_ = 0;
     // claims buffer table
     DevArr<ClaimBuf> claim_bufs_;
@@ -457,7 +458,8 @@ void Engine::allocate(int th, int tw) {
     off_slots_ = (sizeof(FrameDev) + 15) / 16 * 16;
     off_claims_ = off_slots_ + (size_t)slots * sizeof(SlotDev);
     off_fresh_ = off_claims_ + (size_t)max_claims_ * sizeof(int);
-    params_bytes_ = off_fresh_ + slots;
+    off_own_ = off_fresh_ + slots;
+    params_bytes_ = off_own_ + slots;
     params_d_.alloc(params_bytes_);
     for (int i = 0; i < 2; ++i) {
         CUDA_CHECK(cudaMallocHost(&params_hb_[i], params_bytes_));
@@ -468,6 +470,7 @@ void Engine::allocate(int th, int tw) {
     d_slots_ = reinterpret_cast<SlotDev*>(params_d_.p + off_slots_);
     d_claims_ = reinterpret_cast<int*>(params_d_.p + off_claims_);
     d_fresh_ = params_d_.p + off_fresh_;
+    d_own_ = params_d_.p + off_own_;
 
     const size_t nl = net_.layers.size();
     off_dropped_ = nl * 8;
@@ -611,6 +614,14 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
         const int64_t r = t.ty - pl.origin.ty, cc = t.tx - pl.origin.tx;
         if (r >= 0 && r < th && cc >= 0 && cc < tw) hf[r * tw + cc] = 1;
     }
+    // owned map of the placement tiles (TileLedger::holds, buffer_manager.hpp:41-44)
+    uint8_t* ho = params_h_ + off_own_;
+    for (int r = 0; r < th; ++r)
+        for (int cc = 0; cc < tw; ++cc) {
+            const Coord t{pl.origin.tx + cc, pl.origin.ty + r};
+            const auto& sl = slots[ledger_.slot_index(t)];
+            ho[r * tw + cc] = (sl.used && sl.coord.tx == t.tx && sl.coord.ty == t.ty) ? 1 : 0;
+        }
     CUDA_CHECK(cudaMemcpyAsync(params_d_.p, params_h_, params_bytes_, cudaMemcpyHostToDevice, stream_));
     CUDA_CHECK(cudaEventRecord(params_ev_[pslot_], stream_));
     CUDA_CHECK(cudaMemsetAsync(counters_d_.p, 0, cnt_bytes_, stream_));
@@ -686,11 +697,14 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
             case DFX_OUTPUT:
                 if (a.halo > 0) PROF(DFX_FAM_TRUNC, launch_ring_add(C, s, a, rt.aux));
                 {
-                    bool fused = false;
-                    PROF(DFX_FAM_TRUNC, fused = launch_trunc_fused(C, s, a, rt.acc, rt.aux, rt.thr,
-                                                                  l.kind == DFX_RELU ? 1 : 0, rt.pkt));
-                    if (!fused) {
-                        --launches_;
+                    // two streaming passes: tile max, then fire / fold (kernels_hbm.cu)
+                    const int pi = prof_begin(DFX_FAM_TRUNC);
+                    const bool two = launch_trunc_two_pass(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots,
+                                                           rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt);
+                    prof_end(pi);
+                    if (two) {
+                        launches_ += 2;
+                    } else {
                         PROF(DFX_FAM_TRUNC, launch_trunc_max(C, s, a, rt.aux, tmax + (size_t)idx2 * nslots));
                         PROF(DFX_FAM_TRUNC, launch_trunc_apply(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots,
                                                              rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt));
@@ -698,7 +712,9 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                 }
                 break;
             case DFX_MAXPOOL:
-                if (a.halo == 0 && l.pool_k == l.pool_s) {
+                if (a.halo == 0 && l.pool_k == l.pool_s && (a.C & 3) == 0) {
+                    PROF(DFX_FAM_POOL, launch_maxpool_vec(C, s, a, rt.acc, rt.aux, l.pool_k, rt.pkt));
+                } else if (a.halo == 0 && l.pool_k == l.pool_s) {
                     PROF(DFX_FAM_POOL, launch_maxpool_fused(C, s, a, rt.acc, rt.aux, l.pool_k, rt.pkt));
                 } else {
                     PROF(DFX_FAM_POOL, launch_tile_add(C, s, a, rt.acc));

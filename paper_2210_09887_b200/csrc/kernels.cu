@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.hpp"
+#include "pdl.hpp"
 
 namespace dfx {
 
@@ -17,7 +18,11 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// TileLedger::holds (buffer_manager.hpp:41-44): placement tiles read the
+// per-frame owned map (one byte, uploaded with the frame parameters); ring
+// tiles outside the placement read the slot table.
 __device__ __forceinline__ bool holds(const Ctx& c, const FrameDev& F, int qy, int qx) {
+    if (qy >= 0 && qy < F.th && qx >= 0 && qx < F.tw) return c.own[qy * F.tw + qx] != 0;
     const SlotDev& s = c.slots[slot_of(F, c.rows, c.cols, qy, qx)];
     return s.used && s.ty == F.oty + qy && s.tx == F.otx + qx;
 }
@@ -67,6 +72,7 @@ int grid_for(long long n, int per_block = kThreads) {
 // alignment.cpp:58-104, bilinear branch: inverse mapping in double, float weights.
 __global__ void k_warp(Ctx c, const float* __restrict__ frame, int C, float* __restrict__ warped,
                        uint8_t* __restrict__ fp) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int H = F.frame_h, W = F.frame_w;
     const long long n = (long long)H * W;
@@ -105,6 +111,7 @@ __global__ void k_warp(Ctx c, const float* __restrict__ frame, int C, float* __r
 __global__ void k_align(Ctx c, const float* __restrict__ frame, const float* __restrict__ warped,
                         const uint8_t* __restrict__ fp, int C, float* __restrict__ aligned,
                         uint8_t* __restrict__ valid, int pitch, int T) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int ch_ = F.th * T, cw = F.tw * T;
     const long long n = (long long)ch_ * cw;
@@ -132,6 +139,7 @@ __global__ void k_align(Ctx c, const float* __restrict__ frame, const float* __r
 
 // Valid warped pixels that the crop dropped (alignment.cpp:131-164), bilinear path.
 __global__ void k_count_dropped(Ctx c, const uint8_t* __restrict__ fp, int T, unsigned long long* counter) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int H = F.frame_h, W = F.frame_w;
     const long long n = (long long)H * W;
@@ -147,6 +155,7 @@ __global__ void k_count_dropped(Ctx c, const uint8_t* __restrict__ fp, int T, un
 
 // roi_factor_map (alignment.cpp:228-239) via window_max (:198-224), rows pass.
 __global__ void k_roi_rows(Ctx c, const float* __restrict__ roi, float* __restrict__ mid, int pitch, int T) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int eh = F.th * T, ew = F.tw * T;
     const long long n = (long long)eh * ew;
@@ -168,6 +177,7 @@ __global__ void k_roi_rows(Ctx c, const float* __restrict__ roi, float* __restri
 }
 
 __global__ void k_roi_cols(Ctx c, const float* __restrict__ mid, float* __restrict__ fac, int pitch, int T) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int eh = F.th * T, ew = F.tw * T;
     const long long n = (long long)eh * ew;
@@ -193,6 +203,7 @@ __global__ void k_roi_cols(Ctx c, const float* __restrict__ mid, float* __restri
 
 // Tile covered iff any valid pixel (alignment.cpp:179-183).
 __global__ void k_coverage(Ctx c, const uint8_t* __restrict__ valid, int pitch, int T, uint8_t* __restrict__ cov) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int ti = blockIdx.x;
     if (ti >= F.th * F.tw) return;
@@ -210,6 +221,7 @@ __global__ void k_coverage(Ctx c, const uint8_t* __restrict__ valid, int pitch, 
 __global__ void k_input_sig(Ctx c, const float* __restrict__ aligned, const uint8_t* __restrict__ cov, BufDev acc,
                             BufDev trunc, const float* __restrict__ fac, float thr, int pitch, int T,
                             uint8_t* __restrict__ sig) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int eh = F.th * T, ew = F.tw * T;
     const long long n = (long long)eh * ew;
@@ -234,6 +246,7 @@ __global__ void k_input_sig(Ctx c, const float* __restrict__ aligned, const uint
 
 // Supporter rule: keep iff >= 2 significant in the clipped 3x3 (engine.cpp:142-158).
 __global__ void k_noise(Ctx c, const uint8_t* __restrict__ sig, uint8_t* __restrict__ out, int pitch, int T) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int eh = F.th * T, ew = F.tw * T;
     const long long n = (long long)eh * ew;
@@ -259,6 +272,7 @@ __global__ void k_noise(Ctx c, const uint8_t* __restrict__ sig, uint8_t* __restr
 // map, window_max is a binary max filter), or fresh and covered.
 __global__ void k_gate(Ctx c, const uint8_t* __restrict__ sig, const uint8_t* __restrict__ cov,
                        const uint8_t* __restrict__ fresh, int r, int pitch, int T, uint8_t* __restrict__ gate) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int ti = blockIdx.x;
     if (ti >= F.th * F.tw) return;
@@ -295,6 +309,7 @@ __host__ __device__ inline int chunks_per_tile(int t, int C) {
 // trunc = 0, out = cand; else trunc += raw (the reference's double count).
 __global__ void k_input_apply(Ctx c, const float* __restrict__ aligned, const uint8_t* __restrict__ cov,
                               const uint8_t* __restrict__ gate, BufDev acc, BufDev trunc, PktDev out, int pitch) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int T = acc.t, C = acc.C;
     const int nch = chunks_per_tile(T, C), rpc = rows_per_chunk(T, C);
@@ -329,6 +344,7 @@ __global__ void k_input_apply(Ctx c, const float* __restrict__ aligned, const ui
 // Claimed tiles of every buffer: zero, or the bias-init fill for truncated
 // buffers (buffer_manager.cpp:68-89, engine.cpp:78-91; fill after zero == fill).
 __global__ void k_claims(Ctx c, const int* __restrict__ claim_slots, const ClaimBuf* __restrict__ bufs) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int ci = blockIdx.x;
     if (ci >= F.nclaims) return;
@@ -350,6 +366,7 @@ __global__ void k_claims(Ctx c, const int* __restrict__ claim_slots, const Claim
 // Ring ("dilated border") pixels of a packet added into a wrapped buffer at
 // owned slots (delta_layers.cpp:168-183 stash; :262-275 for maxpool acc).
 __global__ void k_ring_add(Ctx c, PktDev in, BufDev dst) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int h = in.halo, t = in.t, C = in.C;
     const int eh = F.th * t, ew = F.tw * t;
@@ -387,6 +404,7 @@ __global__ void k_ring_add(Ctx c, PktDev in, BufDev dst) {
 
 // tile_max of |trunc + delta| over a masked owned tile (delta_layers.cpp:194-201).
 __global__ void k_trunc_max(Ctx c, PktDev in, BufDev trunc, unsigned* __restrict__ tile_max) {
+    pdl_enter();
     __shared__ float red[32];
     const FrameDev& F = *c.f;
     const int T = in.t, C = in.C;
@@ -423,6 +441,7 @@ __global__ void k_trunc_max(Ctx c, PktDev in, BufDev trunc, unsigned* __restrict
 // Fire / fold per masked owned tile (delta_layers.cpp:203-228).
 __global__ void k_trunc_apply(Ctx c, PktDev in, BufDev acc, BufDev trunc, const unsigned* __restrict__ tile_max,
                               float thr, int relu, PktDev out) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int T = in.t, C = in.C;
     const int nch = chunks_per_tile(T, C), rpc = rows_per_chunk(T, C);
@@ -514,6 +533,7 @@ __device__ __forceinline__ float ld_dsmem_f32(const float* local, uint32_t rank)
 
 __global__ void __launch_bounds__(kTruncThreads, 1)
     k_trunc_fused(Ctx c, PktDev in, BufDev acc, BufDev trunc, float thr, int relu, PktDev out, int cs) {
+    pdl_enter();
     __shared__ float red[32];
     __shared__ float s_blockmax;
     const FrameDev& F = *c.f;
@@ -601,6 +621,7 @@ __global__ void __launch_bounds__(kTruncThreads, 1)
 
 // acc += delta on masked owned tiles (delta_layers.cpp:253-261).
 __global__ void k_tile_add(Ctx c, PktDev in, BufDev acc) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int T = in.t, C = in.C;
     const int nch = chunks_per_tile(T, C), rpc = rows_per_chunk(T, C);
@@ -666,6 +687,7 @@ __global__ void __launch_bounds__(256) k_conv_targets(Ctx c, PktDev in, int k, i
                                                       int* __restrict__ list, int* __restrict__ count,
                                                       unsigned long long* __restrict__ flop_px,
                                                       const uint8_t* __restrict__ dense_map, int nux_max) {
+    pdl_enter();
     __shared__ uint32_t s_bits[kTgtMaxPx / 32];
     __shared__ uint8_t s_nb[8][8];
     __shared__ int s_tr0, s_tc0;
@@ -785,6 +807,7 @@ __global__ void __launch_bounds__(256) k_conv_targets(Ctx c, PktDev in, int k, i
 // each masked tile. Targets == all pixels of masked tiles; ownership of the
 // input and output tile is the same slot.
 __global__ void k_maxpool_fused(Ctx c, PktDev in, BufDev acc, BufDev prev, int k, PktDev out) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int to = out.t, ti_ = in.t, C = in.C;
     const int per_tile = to * to * C;
@@ -832,6 +855,7 @@ constexpr int kXP = 32, kXO = 64;
 __global__ void __launch_bounds__(256) k_conv_exact(Ctx c, PktDev in, const float* __restrict__ w, int cin, int cout,
                                                     int k, int s, int r, PktDev out, int hg, const int* __restrict__ list,
                                                     const int* __restrict__ count, int ci_chunk) {
+    pdl_enter();
     extern __shared__ float smem[];
     __shared__ int s_y[kXP], s_x[kXP];
     const FrameDev& F = *c.f;
@@ -899,6 +923,7 @@ __global__ void __launch_bounds__(256) k_conv_exact(Ctx c, PktDev in, const floa
 // accumulated input (first-element init, non-owned tiles read 0), out = m - prev,
 // prev = m, on owned target outputs.
 __global__ void k_maxpool_out(Ctx c, PktDev in, BufDev acc, BufDev prev, int k, int s, PktDev out, int hg) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     int i, j;
     if (!ext_tile(F, out, i, j)) return;
@@ -939,6 +964,7 @@ __global__ void k_maxpool_out(Ctx c, PktDev in, BufDev acc, BufDev prev, int k, 
 
 // Average pool (delta_layers.cpp:320-349): sum in (ky, kx) order times 1/k^2.
 __global__ void k_avgpool(Ctx c, PktDev in, int k, int s, PktDev out) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     int i, j;
     if (!ext_tile(F, out, i, j)) return;
@@ -973,6 +999,7 @@ __global__ void k_avgpool(Ctx c, PktDev in, int k, int s, PktDev out) {
 
 // Nearest upsample (delta_layers.cpp:351-363).
 __global__ void k_upsample(Ctx c, PktDev in, int f, PktDev out) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     int i, j;
     if (!ext_tile(F, out, i, j)) return;
@@ -991,6 +1018,7 @@ __global__ void k_upsample(Ctx c, PktDev in, int f, PktDev out) {
 
 // BatchNorm scale (delta_layers.cpp:365-376).
 __global__ void k_bn(Ctx c, PktDev in, const float* __restrict__ scale, PktDev out) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     int i, j;
     if (!ext_tile(F, out, i, j)) return;
@@ -1013,6 +1041,7 @@ __device__ __forceinline__ bool ext_in_range(const FrameDev& F, const PktDev& p,
 
 // Add: zero-extended sum, mask OR (delta_layers.cpp:378-393).
 __global__ void k_add(Ctx c, PktDev a, PktDev b, PktDev out) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     int i, j;
     if (!ext_tile(F, out, i, j)) return;
@@ -1034,6 +1063,7 @@ __global__ void k_add(Ctx c, PktDev a, PktDev b, PktDev out) {
 
 // Output = acc + trunc over the placement, CHW (delta_layers.cpp:395-400).
 __global__ void k_densify(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ out) {
+    pdl_enter();
     const FrameDev& F = *c.f;
     const int t = acc.t, C = acc.C;
     const int oh = F.th * t, ow = F.tw * t;
@@ -1071,59 +1101,59 @@ static int persistent_grid(long long work) {
 
 void launch_warp(const Ctx& c, cudaStream_t s, const float* frame, int C, float* warped, uint8_t* fp) {
     // frame dims are per-frame but bounded by the staging buffer; use a persistent grid
-    k_warp<<<num_sms_cached() * 8, kThreads, 0, s>>>(c, frame, C, warped, fp);
+    launch_pdl(k_warp, num_sms_cached() * 8, kThreads, 0, s, c, frame, C, warped, fp);
 }
 void launch_align(const Ctx& c, cudaStream_t s, const float* frame, const float* warped, const uint8_t* fp, int C,
                   float* aligned, uint8_t* valid, int pitch, int T) {
-    k_align<<<persistent_grid((long long)c.rows * T * pitch), kThreads, 0, s>>>(c, frame, warped, fp, C, aligned,
+    launch_pdl(k_align, persistent_grid((long long)c.rows * T * pitch), kThreads, 0, s, c, frame, warped, fp, C, aligned,
                                                                                valid, pitch, T);
 }
 void launch_count_dropped(const Ctx& c, cudaStream_t s, const uint8_t* fp, int T, unsigned long long* counter) {
-    k_count_dropped<<<num_sms_cached() * 4, kThreads, 0, s>>>(c, fp, T, counter);
+    launch_pdl(k_count_dropped, num_sms_cached() * 4, kThreads, 0, s, c, fp, T, counter);
 }
 void launch_roi_factor(const Ctx& c, cudaStream_t s, const float* roi, float* tmp3, float* fac, int pitch, int T) {
     const long long n = (long long)c.rows * T * pitch;
-    k_roi_rows<<<persistent_grid(n), kThreads, 0, s>>>(c, roi, tmp3, pitch, T);
-    k_roi_cols<<<persistent_grid(n), kThreads, 0, s>>>(c, tmp3, fac, pitch, T);
+    launch_pdl(k_roi_rows, persistent_grid(n), kThreads, 0, s, c, roi, tmp3, pitch, T);
+    launch_pdl(k_roi_cols, persistent_grid(n), kThreads, 0, s, c, tmp3, fac, pitch, T);
 }
 void launch_coverage(const Ctx& c, cudaStream_t s, const uint8_t* valid, int pitch, int T, uint8_t* cov) {
-    k_coverage<<<c.rows * c.cols, kThreads, 0, s>>>(c, valid, pitch, T, cov);
+    launch_pdl(k_coverage, c.rows * c.cols, kThreads, 0, s, c, valid, pitch, T, cov);
 }
 void launch_input_sig(const Ctx& c, cudaStream_t s, const float* aligned, const uint8_t* cov, BufDev acc,
                       BufDev trunc, const float* fac, float thr, int pitch, int T, uint8_t* sig) {
-    k_input_sig<<<persistent_grid((long long)c.rows * T * pitch), kThreads, 0, s>>>(c, aligned, cov, acc, trunc, fac,
+    launch_pdl(k_input_sig, persistent_grid((long long)c.rows * T * pitch), kThreads, 0, s, c, aligned, cov, acc, trunc, fac,
                                                                                    thr, pitch, T, sig);
 }
 void launch_noise(const Ctx& c, cudaStream_t s, const uint8_t* sig, uint8_t* out, int pitch, int T) {
-    k_noise<<<persistent_grid((long long)c.rows * T * pitch), kThreads, 0, s>>>(c, sig, out, pitch, T);
+    launch_pdl(k_noise, persistent_grid((long long)c.rows * T * pitch), kThreads, 0, s, c, sig, out, pitch, T);
 }
 void launch_gate(const Ctx& c, cudaStream_t s, const uint8_t* sig, const uint8_t* cov, const uint8_t* fresh,
                  int dilation, int pitch, int T, uint8_t* gate) {
-    k_gate<<<c.rows * c.cols, kThreads, 0, s>>>(c, sig, cov, fresh, dilation, pitch, T, gate);
+    launch_pdl(k_gate, c.rows * c.cols, kThreads, 0, s, c, sig, cov, fresh, dilation, pitch, T, gate);
 }
 void launch_input_apply(const Ctx& c, cudaStream_t s, const float* aligned, const uint8_t* cov, const uint8_t* gate,
                         BufDev acc, BufDev trunc, PktDev out, int pitch) {
     const int nch = chunks_per_tile(acc.t, acc.C);
-    k_input_apply<<<c.rows * c.cols * nch, kThreads, 0, s>>>(c, aligned, cov, gate, acc, trunc, out, pitch);
+    launch_pdl(k_input_apply, c.rows * c.cols * nch, kThreads, 0, s, c, aligned, cov, gate, acc, trunc, out, pitch);
 }
 void launch_claims(const Ctx& c, cudaStream_t s, const int* claim_slots, const ClaimBuf* bufs, int nbuf,
                    int max_claims) {
     if (nbuf <= 0 || max_claims <= 0) return;
-    k_claims<<<dim3(max_claims, nbuf), kThreads, 0, s>>>(c, claim_slots, bufs);
+    launch_pdl(k_claims, dim3(max_claims, nbuf), kThreads, 0, s, c, claim_slots, bufs);
 }
 void launch_ring_add(const Ctx& c, cudaStream_t s, PktDev in, BufDev dst) {
     if (in.halo <= 0) return;
     const long long n = (2LL * in.halo * (c.cols * in.t + 2 * in.halo) + 2LL * c.rows * in.t * in.halo) * in.C;
-    k_ring_add<<<persistent_grid(n), kThreads, 0, s>>>(c, in, dst);
+    launch_pdl(k_ring_add, persistent_grid(n), kThreads, 0, s, c, in, dst);
 }
 void launch_trunc_max(const Ctx& c, cudaStream_t s, PktDev in, BufDev trunc, unsigned* tile_max) {
     const int nch = chunks_per_tile(in.t, in.C);
-    k_trunc_max<<<c.rows * c.cols * nch, kThreads, 0, s>>>(c, in, trunc, tile_max);
+    launch_pdl(k_trunc_max, c.rows * c.cols * nch, kThreads, 0, s, c, in, trunc, tile_max);
 }
 void launch_trunc_apply(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, const unsigned* tile_max,
                         float thr, int relu, PktDev out) {
     const int nch = chunks_per_tile(in.t, in.C);
-    k_trunc_apply<<<c.rows * c.cols * nch, kThreads, 0, s>>>(c, in, acc, trunc, tile_max, thr, relu, out);
+    launch_pdl(k_trunc_apply, c.rows * c.cols * nch, kThreads, 0, s, c, in, acc, trunc, tile_max, thr, relu, out);
 }
 bool launch_trunc_fused(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, float thr, int relu,
                         PktDev out) {
@@ -1148,33 +1178,33 @@ bool launch_trunc_fused(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, Buf
 }
 void launch_tile_add(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc) {
     const int nch = chunks_per_tile(in.t, in.C);
-    k_tile_add<<<c.rows * c.cols * nch, kThreads, 0, s>>>(c, in, acc);
+    launch_pdl(k_tile_add, c.rows * c.cols * nch, kThreads, 0, s, c, in, acc);
 }
 static int ext_blocks(const Ctx& c, const PktDev& out) { return (c.rows + 2 * out.RT) * (c.cols + 2 * out.RT); }
 void launch_maxpool_out(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, int st, PktDev out,
                         int hg) {
-    k_maxpool_out<<<ext_blocks(c, out), kThreads, 0, s>>>(c, in, acc, prev, k, st, out, hg);
+    launch_pdl(k_maxpool_out, ext_blocks(c, out), kThreads, 0, s, c, in, acc, prev, k, st, out, hg);
 }
 void launch_maxpool_fused(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, PktDev out) {
     const int nch = (out.t * out.t * in.C + 4095) / 4096;
-    k_maxpool_fused<<<c.rows * c.cols * nch, kThreads, 0, s>>>(c, in, acc, prev, k, out);
+    launch_pdl(k_maxpool_fused, c.rows * c.cols * nch, kThreads, 0, s, c, in, acc, prev, k, out);
 }
 void launch_avgpool(const Ctx& c, cudaStream_t s, PktDev in, int k, int st, PktDev out) {
-    k_avgpool<<<ext_blocks(c, out), kThreads, 0, s>>>(c, in, k, st, out);
+    launch_pdl(k_avgpool, ext_blocks(c, out), kThreads, 0, s, c, in, k, st, out);
 }
 void launch_upsample(const Ctx& c, cudaStream_t s, PktDev in, int f, PktDev out) {
-    k_upsample<<<ext_blocks(c, out), kThreads, 0, s>>>(c, in, f, out);
+    launch_pdl(k_upsample, ext_blocks(c, out), kThreads, 0, s, c, in, f, out);
 }
 void launch_bn(const Ctx& c, cudaStream_t s, PktDev in, const float* scale, PktDev out) {
-    k_bn<<<ext_blocks(c, out), kThreads, 0, s>>>(c, in, scale, out);
+    launch_pdl(k_bn, ext_blocks(c, out), kThreads, 0, s, c, in, scale, out);
 }
 void launch_add(const Ctx& c, cudaStream_t s, PktDev a, PktDev b, PktDev out) {
-    k_add<<<ext_blocks(c, out), kThreads, 0, s>>>(c, a, b, out);
+    launch_pdl(k_add, ext_blocks(c, out), kThreads, 0, s, c, a, b, out);
 }
 void launch_conv_targets(const Ctx& c, cudaStream_t s, PktDev in, int k, int st, int r, PktDev out, int hg, int* list,
                          int* count, unsigned long long* flop_px, const uint8_t* dense_map, int nux_max) {
     const int RTg = (hg + out.t - 1) / out.t;
-    k_conv_targets<<<(c.rows + 2 * RTg) * (c.cols + 2 * RTg), kThreads, 0, s>>>(c, in, k, st, r, out, hg, list, count,
+    launch_pdl(k_conv_targets, (c.rows + 2 * RTg) * (c.cols + 2 * RTg), kThreads, 0, s, c, in, k, st, r, out, hg, list, count,
                                                                                 flop_px, dense_map, nux_max);
 }
 void launch_conv_exact(const Ctx& c, cudaStream_t s, PktDev in, const float* w, int cin, int cout, int k, int st, int r,
@@ -1188,10 +1218,10 @@ void launch_conv_exact(const Ctx& c, cudaStream_t s, PktDev in, const float* w, 
     long long g = num_sms_cached() * 4;
     if (items < g) g = items;
     if (g < 1) g = 1;
-    k_conv_exact<<<(int)g, 256, smem, s>>>(c, in, w, cin, cout, k, st, r, out, hg, list, count, ci);
+    launch_pdl(k_conv_exact, (int)g, 256, smem, s, c, in, w, cin, cout, k, st, r, out, hg, list, count, ci);
 }
 void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out) {
-    k_densify<<<persistent_grid((long long)acc.C * c.rows * acc.t * c.cols * acc.t), kThreads, 0, s>>>(c, acc, trunc,
+    launch_pdl(k_densify, persistent_grid((long long)acc.C * c.rows * acc.t * c.cols * acc.t), kThreads, 0, s, c, acc, trunc,
                                                                                                        out);
 }
 

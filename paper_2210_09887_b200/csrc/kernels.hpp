@@ -13,6 +13,7 @@ struct Ctx {
     const FrameDev* f;     // device
     const SlotDev* slots;  // device [rows*cols]
     int rows, cols;
+    const uint8_t* own;    // device [th*tw]: placement tile owns its slot (TileLedger::holds)
 };
 
 struct ClaimBuf {
@@ -48,6 +49,10 @@ void launch_trunc_max(const Ctx& c, cudaStream_t s, PktDev in, BufDev trunc, uns
 // cluster); returns false when the shape needs the two-pass fallback.
 bool launch_trunc_fused(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, float thr, int relu,
                         PktDev out);
+// Two streaming passes (kernels_hbm.cu): tile max, then fire / fold. Needs C % 4 == 0.
+bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
+                           float thr, int relu, PktDev out);
+bool launch_maxpool_vec(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, PktDev out);
 void launch_trunc_apply(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
                         const unsigned* tile_max, float thr, int relu, PktDev out);
 

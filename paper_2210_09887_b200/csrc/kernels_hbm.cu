@@ -1,0 +1,294 @@
+// Streaming (HBM-bound) kernels of the delta activation and max pooling,
+// written for bandwidth: warps are the work units, each takes a 16 KB chunk of
+// a masked tile, every access is a 16-byte vector, and a persistent grid keeps
+// ~64 warps per SM with several KB of loads in flight each. A work item is
+// 4 KB of one tile (one round of 8 float4 per lane), so even a few masked
+// tiles spread over every SM.
+//
+// Truncation (delta_activation_truncate, reference src/delta_layers.cpp:
+// 185-228) needs the max over a WHOLE tile before any write, so it is two
+// passes:
+//   k_trunc_tilemax  max |trunc + delta| per masked owned tile (read only,
+//                    atomicMax on the float bits: values are >= 0);
+//   k_trunc_commit   fire (acc += trunc + delta, trunc = 0, out = relu(acc') -
+//                    relu(acc) or the candidate) or fold (trunc += delta).
+// The second pass re-reads trunc and delta from L2 (a layer's masked tiles are
+// far smaller than the 126 MB L2), so DRAM sees the algorithmic traffic.
+// Arithmetic is the reference's fp32 order with explicit rounding intrinsics.
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+#include "pdl.hpp"
+
+namespace dfx {
+
+namespace {
+
+constexpr int kSub = 8;               // float4s per lane in flight per array
+constexpr int kChunkF4 = 32 * kSub;   // float4s per warp work item (4 KB): one round, all loads issued up front
+
+// Placement tile (qy, qx) owns its slot (TileLedger::holds, buffer_manager.hpp:41-44).
+__device__ __forceinline__ bool holds_t(const Ctx& c, const FrameDev& F, int qy, int qx) {
+    return c.own[qy * F.tw + qx] != 0;
+}
+__device__ __forceinline__ float* tile_base(const Ctx& c, const FrameDev& F, BufDev b, int qy, int qx) {
+    return b.d + (size_t)slot_of(F, c.rows, c.cols, qy, qx) * b.t * b.t * b.C;
+}
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+    return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ float amax4(float m, float4 v) {
+    return fmaxf(fmaxf(fmaxf(m, fabsf(v.x)), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+}
+
+// Masked (and, if own, owned) placement tiles of packet p, in tile order, into
+// shared memory: one ballot + prefix per 256 tiles. Returns the count, or -1
+// when the placement has more tiles than the list holds (callers then test
+// every tile).
+constexpr int kMaxList = 2048;
+__device__ int build_tile_list(const Ctx& c, const FrameDev& F, const PktDev& p, bool own, int* s_list, int* s_warp) {
+    const int nt = F.th * F.tw;
+    if (nt > kMaxList) return -1;
+    // each thread owns up to 8 consecutive tiles: all loads in one round
+    constexpr int kPer = kMaxList / 256;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int t0 = threadIdx.x * kPer;
+    unsigned bits = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int ti = t0 + j;
+        if (ti < nt) {
+            const int tr = ti / F.tw, tc = ti - tr * F.tw;
+            if (p.ext[ext_idx(p, tr, tc)] != 0 && (!own || c.own[ti] != 0)) bits |= 1u << j;
+        }
+    }
+    // block exclusive prefix of the per-thread counts
+    int v = __popc(bits), incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[w] = incl;
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int j = 0; j < nwb; ++j) {
+        off += j < w ? s_warp[j] : 0;
+        tot += s_warp[j];
+    }
+    off += incl - v;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+        if (bits >> j & 1u) s_list[off++] = t0 + j;
+    __syncthreads();
+    return tot;
+}
+
+// Delta packet float4 of tile element e4 (tile row-major [yy][xx][c]).
+__device__ __forceinline__ const float4* pkt_f4(const PktDev& p, int tr, int tc, int e4, int row4) {
+    const int yy = e4 / row4, rem = e4 - yy * row4;
+    return reinterpret_cast<const float4*>(p.d + pkt_off(p, tr * p.t + yy, tc * p.t)) + rem;
+}
+
+__global__ void __launch_bounds__(256) k_trunc_tilemax(Ctx c, PktDev in, BufDev trunc, unsigned* __restrict__ tile_max) {
+    pdl_enter();
+    __shared__ int s_list[kMaxList];
+    __shared__ int s_warp[8];
+    const FrameDev& F = *c.f;
+    const int T = in.t, E4 = T * T * in.C / 4, row4 = T * in.C / 4;
+    const int nch = (E4 + kChunkF4 - 1) / kChunkF4;
+    const int nl = build_tile_list(c, F, in, true, s_list, s_warp);
+    const int items = (nl < 0 ? F.th * F.tw : nl) * nch;
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int it = gw; it < items; it += nw) {
+        const int li = it / nch, ch = it - li * nch;
+        const int ti = nl < 0 ? li : s_list[li];
+        const int tr = ti / F.tw, tc = ti - tr * F.tw;
+        if (nl < 0 && (!in.ext[ext_idx(in, tr, tc)] || !holds_t(c, F, tr, tc))) continue;
+        const float4* tb = reinterpret_cast<const float4*>(tile_base(c, F, trunc, tr, tc));
+        const int q0 = ch * kChunkF4, q1 = min(E4, q0 + kChunkF4);
+        float m = 0.0f;
+        for (int qs = q0; qs < q1; qs += 32 * kSub) {
+            float4 tv[kSub], dv[kSub];
+#pragma unroll
+            for (int j = 0; j < kSub; ++j) {
+                const int q = qs + j * 32 + lane;
+                if (q < q1) {
+                    tv[j] = __ldcg(tb + q);
+                    dv[j] = __ldcg(pkt_f4(in, tr, tc, q, row4));
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kSub; ++j)
+                if (qs + j * 32 + lane < q1) m = amax4(m, add4(tv[j], dv[j]));
+        }
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0 && m > 0.0f) atomicMax(tile_max + ti, __float_as_uint(m));
+    }
+}
+
+__global__ void __launch_bounds__(256) k_trunc_commit(Ctx c, PktDev in, BufDev acc, BufDev trunc,
+                                                      const unsigned* __restrict__ tile_max, float thr, int relu,
+                                                      PktDev out) {
+    pdl_enter();
+    __shared__ int s_list[kMaxList];
+    __shared__ int s_warp[8];
+    const FrameDev& F = *c.f;
+    const int T = in.t, E4 = T * T * in.C / 4, row4 = T * in.C / 4;
+    const int nch = (E4 + kChunkF4 - 1) / kChunkF4;
+    // output mask = fired tiles (delta_layers.cpp:203-204), every placement tile
+    for (int ti = blockIdx.x * blockDim.x + threadIdx.x; ti < F.th * F.tw; ti += gridDim.x * blockDim.x) {
+        const int tr = ti / F.tw, tc = ti - tr * F.tw;
+        const float tm = __uint_as_float(tile_max[ti]);
+        out.ext[ext_idx(out, tr, tc)] =
+            (in.ext[ext_idx(in, tr, tc)] && holds_t(c, F, tr, tc) && tm >= thr && tm > 0.0f) ? 1 : 0;
+    }
+    const int nl = build_tile_list(c, F, in, true, s_list, s_warp);
+    const int items = (nl < 0 ? F.th * F.tw : nl) * nch;
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int it = gw; it < items; it += nw) {
+        const int li = it / nch, ch = it - li * nch;
+        const int ti = nl < 0 ? li : s_list[li];
+        const int tr = ti / F.tw, tc = ti - tr * F.tw;
+        if (nl < 0 && (!in.ext[ext_idx(in, tr, tc)] || !holds_t(c, F, tr, tc))) continue;
+        const float tm = __uint_as_float(tile_max[ti]);
+        const bool fire = tm >= thr && tm > 0.0f;
+        float4* tb = reinterpret_cast<float4*>(tile_base(c, F, trunc, tr, tc));
+        float4* ab = reinterpret_cast<float4*>(tile_base(c, F, acc, tr, tc));
+        const int q0 = ch * kChunkF4, q1 = min(E4, q0 + kChunkF4);
+        for (int qs = q0; qs < q1; qs += 32 * kSub) {
+            constexpr int kS = kSub / 2;  // three arrays in flight: keep registers (occupancy) in check
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+            float4 tv[kS], dv[kS], pv[kS];
+#pragma unroll
+            for (int j = 0; j < kS; ++j) {
+                const int q = qs + (h * kS + j) * 32 + lane;
+                if (q < q1) {
+                    tv[j] = __ldcg(tb + q);
+                    dv[j] = __ldcg(pkt_f4(in, tr, tc, q, row4));
+                    if (fire) pv[j] = __ldcs(ab + q);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kS; ++j) {
+                const int q = qs + (h * kS + j) * 32 + lane;
+                if (q >= q1) continue;
+                const float4 cd = add4(tv[j], dv[j]);
+                if (fire) {
+                    const float4 nv = add4(pv[j], cd);
+                    float4 o = cd;
+                    if (relu) {
+                        o.x = __fsub_rn(fmaxf(nv.x, 0.f), fmaxf(pv[j].x, 0.f));
+                        o.y = __fsub_rn(fmaxf(nv.y, 0.f), fmaxf(pv[j].y, 0.f));
+                        o.z = __fsub_rn(fmaxf(nv.z, 0.f), fmaxf(pv[j].z, 0.f));
+                        o.w = __fsub_rn(fmaxf(nv.w, 0.f), fmaxf(pv[j].w, 0.f));
+                    }
+                    __stcs(ab + q, nv);
+                    __stcs(tb + q, make_float4(0.f, 0.f, 0.f, 0.f));
+                    const int yy = q / row4, rem = q - yy * row4;
+                    reinterpret_cast<float4*>(out.d + pkt_off(out, tr * T + yy, tc * T))[rem] = o;
+                } else {
+                    __stcs(tb + q, cd);
+                }
+            }
+            }
+        }
+    }
+}
+
+// Max pool, halo-free input, k == stride (network.cpp:164-166), C % 4 == 0:
+// acc += delta over the window (delta_layers.cpp:253-261), window max of acc
+// initialised from the first element (:294-306), out = max - prev, prev = max
+// (:308-310); outputs of masked, non-owned tiles are 0. Work unit: a warp takes
+// a chunk of a masked tile's output float4s.
+__global__ void __launch_bounds__(256) k_maxpool_vec(Ctx c, PktDev in, BufDev acc, BufDev prev, int k, PktDev out) {
+    pdl_enter();
+    __shared__ int s_list[kMaxList];
+    __shared__ int s_warp[8];
+    const FrameDev& F = *c.f;
+    const int to = out.t, ti_ = in.t, C4 = in.C / 4;
+    const int E4 = to * to * C4;
+    const int nch = (E4 + 63) / 64;
+    for (int ti = blockIdx.x * blockDim.x + threadIdx.x; ti < F.th * F.tw; ti += gridDim.x * blockDim.x) {
+        const int tr = ti / F.tw, tc = ti - tr * F.tw;
+        out.ext[ext_idx(out, tr, tc)] = in.ext[ext_idx(in, tr, tc)] ? 1 : 0;
+    }
+    const int nl = build_tile_list(c, F, in, false, s_list, s_warp);
+    const int items = (nl < 0 ? F.th * F.tw : nl) * nch;
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int it = gw; it < items; it += nw) {
+        const int li = it / nch, ch = it - li * nch;
+        const int tix = nl < 0 ? li : s_list[li];
+        const int tr = tix / F.tw, tc = tix - tr * F.tw;
+        if (nl < 0 && !in.ext[ext_idx(in, tr, tc)]) continue;
+        const bool owned = holds_t(c, F, tr, tc);
+        float4* ab = owned ? reinterpret_cast<float4*>(tile_base(c, F, acc, tr, tc)) : nullptr;
+        float4* pb = owned ? reinterpret_cast<float4*>(tile_base(c, F, prev, tr, tc)) : nullptr;
+        const int q0 = ch * 64, q1 = min(E4, q0 + 64);
+#pragma unroll 2
+        for (int q = q0 + lane; q < q1; q += 32) {
+            const int px = q / C4, c4 = q - px * C4;
+            const int y = px / to, x = px - y * to;
+            float4* d = reinterpret_cast<float4*>(out.d + pkt_off(out, tr * to + y, tc * to + x)) + c4;
+            if (!owned) {
+                *d = make_float4(0.f, 0.f, 0.f, 0.f);
+                continue;
+            }
+            float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int ky = 0; ky < k; ++ky)
+                for (int kx = 0; kx < k; ++kx) {
+                    const int iy = y * k + ky, ix = x * k + kx;
+                    float4* ap = ab + ((size_t)iy * ti_ + ix) * C4 + c4;
+                    const float4 dv = __ldcg(reinterpret_cast<const float4*>(in.d + pkt_off(in, tr * ti_ + iy, tc * ti_ + ix)) + c4);
+                    const float4 v = add4(__ldcs(ap), dv);
+                    __stcs(ap, v);
+                    if (ky == 0 && kx == 0) {
+                        m = v;
+                    } else {  // std::max(m, v) == (m < v) ? v : m
+                        m.x = m.x < v.x ? v.x : m.x;
+                        m.y = m.y < v.y ? v.y : m.y;
+                        m.z = m.z < v.z ? v.z : m.z;
+                        m.w = m.w < v.w ? v.w : m.w;
+                    }
+                }
+            float4* pp = pb + ((size_t)y * to + x) * C4 + c4;
+            const float4 pv = __ldcs(pp);
+            *d = make_float4(__fsub_rn(m.x, pv.x), __fsub_rn(m.y, pv.y), __fsub_rn(m.z, pv.z), __fsub_rn(m.w, pv.w));
+            __stcs(pp, m);
+        }
+    }
+}
+
+// Persistent grid: SMs x resident CTAs per SM for this kernel.
+template <typename K>
+int stream_grid(K kernel) {
+    int dev = 0, sms = 148, per = 1;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, 256, 0);
+    return sms * (per < 1 ? 1 : per);
+}
+
+}  // namespace
+
+bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
+                           float thr, int relu, PktDev out) {
+    if ((in.C & 3) != 0) return false;
+    static const int g1 = stream_grid(k_trunc_tilemax), g2 = stream_grid(k_trunc_commit);
+    launch_pdl(k_trunc_tilemax, g1, 256, 0, s, c, in, trunc, tile_max);
+    launch_pdl(k_trunc_commit, g2, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out);
+    return true;
+}
+
+bool launch_maxpool_vec(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, PktDev out) {
+    if ((in.C & 3) != 0) return false;
+    static const int g = stream_grid(k_maxpool_vec);
+    launch_pdl(k_maxpool_vec, g, 256, 0, s, c, in, acc, prev, k, out);
+    return true;
+}
+
+}  // namespace dfx
