@@ -247,32 +247,41 @@ def run_ours(args):
     ms_max = float(ms_t.item())
     value = world * K / (ms_max / 1000.0)
 
-    # ---- 2. e2e through the public API: pinned host frames, H2D + D2H inside the timed region
-    pinned = []
-    for f, _ in seq:
-        t = torch.empty(f.shape, dtype=torch.float32, pin_memory=True)
-        t.numpy()[...] = f
-        pinned.append(t)
+    # ---- 2. e2e through the public API: pinned host frames in, pinned host outputs back; every
+    # step's H2D frame copy and D2H output copy are inside the timed region (pipelined host-frame
+    # API, dfx_engine_submit_host_frame: copies overlap the neighbouring frames' compute)
+    from paper_2210_09887_b200 import _capi
+    import ctypes
+    _, capi = _capi.load_library()
+    fbytes = seq[0][0].nbytes
+    hframes = []
+    for f, _ in seq:  # page-locked host frames (dfx_host_alloc), filled before the timed region
+        p = capi["host_alloc"](fbytes)
+        ctypes.memmove(p, np.ascontiguousarray(f).ctypes.data, fbytes)
+        hframes.append(p)
     eng2 = dfx.DeltaEngine(spec, econf, device=local)
-    infos = []
     for k in range(W):
-        eng2.run_frame_full(pinned[k].numpy(), seq[k][1])
+        eng2.run_frame_full(seq[k][0], seq[k][1])
+    oc, oh, ow = eng2.last_info["out_channels"], eng2.last_info["out_height"], eng2.last_info["out_width"]
+    ocap = oc * (oh + 64) * (ow + 64)
+    houts = [capi["host_alloc"](ocap * 4) for _ in range(2)]
     if dist:
         dist.barrier()
     eng2.timer_start()
+    t_wall = time.time()
     out_bytes = 0
     for k in range(W, W + K):
-        info, out = eng2.run_frame_full(pinned[k].numpy(), seq[k][1])
-        infos.append(info)
-        out_bytes += out.nbytes
+        eng2.submit_host_frame(hframes[k], *seq[k][0].shape, seq[k][1], houts[k & 1], ocap)
+        out_bytes += oc * oh * ow * 4
+    eng2.sync()
     ms2 = eng2.timer_stop()
+    ms2 = max(ms2, (time.time() - t_wall) * 1e3)
+    for p in hframes + houts:
+        capi["host_free"](p)
     ms2_t = torch.tensor([ms2], device=dev)
     if dist:
         dist.all_reduce(ms2_t, op=dist.ReduceOp.MAX)
     e2e_value = world * K / (float(ms2_t.item()) / 1000.0)
-    update_rate = float(np.mean([i["update_rate"] for i in infos]))
-    conv_gflop = float(np.mean([i["conv_flops"] for i in infos])) / 1e9
-    dense_gflop = float(np.mean([i["dense_flops"] for i in infos])) / 1e9
 
     # ---- 3. per-family kernel times (CUDA events on the engine stream) + algorithmic work
     eng3 = dfx.DeltaEngine(spec, econf, device=local)
@@ -281,10 +290,14 @@ def run_ours(args):
         eng3.sync()
     eng3.set_profiling(True)
     eng3.reset_profile()
+    infos = []
     for k in range(W, W + K):
         eng3.submit_frame(dframes[k].data_ptr(), *dframes[k].shape, seq[k][1])
-        eng3.sync()
+        infos.append(eng3.sync())
     prof = eng3.profile()
+    update_rate = float(np.mean([i["update_rate"] for i in infos]))
+    conv_gflop = float(np.mean([i["conv_flops"] for i in infos])) / 1e9
+    dense_gflop = float(np.mean([i["dense_flops"] for i in infos])) / 1e9
     hbm_peak, bf16_peak, peak_src, tf32_peak, tf32_src = load_peaks()
     tc_peak = tf32_peak / 3.0  # 3xTF32: 3 MMA passes per algorithmic FLOP
     kernels = {}

@@ -11,6 +11,7 @@
  *   dfx_engine_run_frame     DeltaEngine::run_frame(frame, h, roi)      engine.hpp:51, engine.cpp:184-287;
  *                            python: deltaflux._core.DeltaEngine.run_frame  bindings/py_bindings.cpp:103-121
  *   dfx_engine_submit_frame  (async variant of run_frame for throughput; no reference counterpart)
+ *   dfx_engine_submit_host_frame (pipelined host-buffer variant of run_frame; no reference counterpart)
  *   dfx_engine_sync          (completes submitted frames)
  *   dfx_engine_reset         DeltaEngine::reset()                      engine.hpp:55, engine.cpp:93-108
  *   dfx_engine_input_mask    FrameResult::input_mask                    engine.hpp:38
@@ -161,7 +162,18 @@ int dfx_engine_run_frame(dfx_engine* e, const float* frame, int c, int h, int w,
  * dfx_engine_sync. */
 int dfx_engine_submit_frame(dfx_engine* e, const float* frame_dev, int c, int h, int w,
                             const float* h9);
+/* Pipelined host-buffer frame (throughput form of dfx_engine_run_frame): the
+ * frame's host->device copy and the densified output's device->host copy into
+ * `out` (CHW, when out_cap is large enough) run on a copy stream overlapping
+ * the compute of neighbouring frames; returns without waiting. `frame` and
+ * `out` should be pinned host memory and must stay untouched until
+ * dfx_engine_sync. */
+int dfx_engine_submit_host_frame(dfx_engine* e, const float* frame, int c, int h, int w, const float* h9, float* out,
+                                 size_t out_cap);
 int dfx_engine_sync(dfx_engine* e, dfx_frame_info* info);
+/* Page-locked host buffers for the pipelined host-frame path (NULL on failure). */
+void* dfx_host_alloc(size_t bytes);
+void dfx_host_free(void* p);
 
 int dfx_engine_reset(dfx_engine* e);
 

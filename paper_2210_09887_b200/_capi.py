@@ -170,6 +170,8 @@ def load_library():
         api[name] = fn
     for name, res, args in [
         ("submit_frame", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, _fp]),
+        ("submit_host_frame", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, _fp, C.c_void_p,
+                                        C.c_size_t]),
         ("sync", C.c_int, [C.c_void_p, C.POINTER(FrameInfo)]),
         ("output_device", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int),
                                     C.POINTER(C.c_int), C.POINTER(C.c_int)]),
@@ -187,6 +189,14 @@ def load_library():
         fn.restype = res
         fn.argtypes = args
         api[name] = fn
+    fn = lib.dfx_host_alloc
+    fn.restype = C.c_void_p
+    fn.argtypes = [C.c_size_t]
+    api["host_alloc"] = fn
+    fn = lib.dfx_host_free
+    fn.restype = None
+    fn.argtypes = [C.c_void_p]
+    api["host_free"] = fn
     fn = lib.dfx_kernel_family_name
     fn.restype = C.c_char_p
     fn.argtypes = [C.c_int]

@@ -133,6 +133,7 @@ class Engine {
     void run_frame(const float* frame, int c, int h, int w, const float* h9, const float* roi, dfx_frame_info* info,
                    float* out, size_t cap);
     void submit(const float* frame_dev, int c, int h, int w, const float* h9);
+    void submit_host(const float* frame, int c, int h, int w, const float* h9, float* out, size_t cap);
     void sync(dfx_frame_info* info);
     void reset();
 
@@ -228,8 +229,16 @@ class Engine {
     DevArr<uint8_t> counters_d_;
     size_t cnt_bytes_ = 0, off_dropped_ = 0, off_counts_ = 0, off_ucounts_ = 0, off_tmax_ = 0;
     uint8_t* readback_h_ = nullptr;  // pinned: flop_px, dropped, input mask
-    // output
+    float *in_h_ = nullptr, *out_h_ = nullptr;  // pinned staging of run_frame's caller buffers
+    size_t in_h_n_ = 0, out_h_n_ = 0;
+    // output (out_cur_: the buffer this frame's densify writes)
     DevArr<float> out_d_;
+    float* out_cur_ = nullptr;
+    // pipelined host path (submit_host): copy stream, double-buffered frame / output
+    cudaStream_t cstream_ = nullptr, dstream_ = nullptr;  // host->device, device->host copies
+    DevArr<float> hframe_d_[2], hout_d_[2];
+    cudaEvent_t ev_h2d_[2] = {nullptr, nullptr}, ev_done_[2] = {nullptr, nullptr}, ev_d2h_[2] = {nullptr, nullptr};
+    uint64_t hseq_ = 0;
     // last frame
     Placement place_{};
     dfx_frame_info pending_{};
@@ -281,6 +290,17 @@ Engine::~Engine() {
         if (params_ev_[i]) cudaEventDestroy(params_ev_[i]);
     }
     if (readback_h_) cudaFreeHost(readback_h_);
+    if (in_h_) cudaFreeHost(in_h_);
+    if (out_h_) cudaFreeHost(out_h_);
+    if (cstream_) cudaStreamSynchronize(cstream_);
+    if (dstream_) cudaStreamSynchronize(dstream_);
+    for (int i = 0; i < 2; ++i) {
+        if (ev_h2d_[i]) cudaEventDestroy(ev_h2d_[i]);
+        if (ev_done_[i]) cudaEventDestroy(ev_done_[i]);
+        if (ev_d2h_[i]) cudaEventDestroy(ev_d2h_[i]);
+    }
+    if (cstream_) cudaStreamDestroy(cstream_);
+    if (dstream_) cudaStreamDestroy(dstream_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -729,7 +749,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
         }
     }
     const LayerRT& ort = lrt_[net_.out_layer];
-    PROF(DFX_FAM_DENSIFY, launch_densify(C, s, ort.acc, ort.aux, out_d_.p));
+    PROF(DFX_FAM_DENSIFY, launch_densify(C, s, ort.acc, ort.aux, out_cur_ ? out_cur_ : out_d_.p));
     CUDA_CHECK(cudaGetLastError());
 
     // small readback: per-layer target counts, dropped, fired input tiles
@@ -919,7 +939,15 @@ void Engine::run_frame(const float* frame, int c, int h, int w, const float* h9,
     CUDA_CHECK(cudaSetDevice(device_));
     const size_t fsz = (size_t)c * h * w;
     ensure_staging(c, h, w, true);
-    CUDA_CHECK(cudaMemcpyAsync(frame_d_.p, frame, fsz * 4, cudaMemcpyHostToDevice, stream_));
+    // caller buffers are ordinary (pageable) host memory: stage through pinned
+    // buffers so the copies run at full PCIe rate
+    if (in_h_n_ < fsz) {
+        if (in_h_) cudaFreeHost(in_h_);
+        CUDA_CHECK(cudaMallocHost(&in_h_, fsz * 4));
+        in_h_n_ = fsz;
+    }
+    memcpy(in_h_, frame, fsz * 4);
+    CUDA_CHECK(cudaMemcpyAsync(frame_d_.p, in_h_, fsz * 4, cudaMemcpyHostToDevice, stream_));
     const float* roi_dev = nullptr;
     if (roi && cfg_.roi_enabled) {
         CUDA_CHECK(cudaMemcpyAsync(roi_frame_d_.p, roi, (size_t)h * w * 4, cudaMemcpyHostToDevice, stream_));
@@ -927,12 +955,19 @@ void Engine::run_frame(const float* frame, int c, int h, int w, const float* h9,
     }
     enqueue(frame_d_.p, c, h, w, h9, roi_dev);
     const size_t n = (size_t)pending_.out_channels * pending_.out_height * pending_.out_width;
-    if (out && cap >= n) {
+    const bool want = out && cap >= n;
+    if (want) {
+        if (out_h_n_ < n) {
+            if (out_h_) cudaFreeHost(out_h_);
+            CUDA_CHECK(cudaMallocHost(&out_h_, n * 4));
+            out_h_n_ = n;
+        }
         // out_d_ is [C][th*t][tw*t] compact (k_densify writes the placement extent)
-        CUDA_CHECK(cudaMemcpyAsync(out, out_d_.p, n * 4, cudaMemcpyDeviceToHost, stream_));
+        CUDA_CHECK(cudaMemcpyAsync(out_h_, out_d_.p, n * 4, cudaMemcpyDeviceToHost, stream_));
     }
     CUDA_CHECK(cudaStreamSynchronize(stream_));
     CUDA_CHECK(cudaGetLastError());
+    if (want) memcpy(out, out_h_, n * 4);
     finish_info(info);
     prof_harvest();
 }
@@ -948,8 +983,55 @@ void Engine::submit(const float* frame_dev, int c, int h, int w, const float* h9
     enqueue(frame_dev, c, h, w, h9, nullptr);
 }
 
+// Pipelined host-buffer frame (throughput form of run_frame): frame k's H2D
+// copy (copy stream 1) overlaps frame k-1's compute, its output D2H copy (copy
+// stream 2) overlaps frame k+1's compute; device frame and output buffers are
+// double buffered and guarded by per-slot events. `frame` and `out` should be
+// pinned for the copies to be asynchronous. Results of the last frame are
+// readable after sync().
+void Engine::submit_host(const float* frame, int c, int h, int w, const float* h9, float* out, size_t cap) {
+    CUDA_CHECK(cudaSetDevice(device_));
+    check(c == net_.in_channels, "run_frame: input channel mismatch");
+    if (!cstream_) {
+        CUDA_CHECK(cudaStreamCreateWithFlags(&cstream_, cudaStreamNonBlocking));
+        CUDA_CHECK(cudaStreamCreateWithFlags(&dstream_, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CUDA_CHECK(cudaEventCreateWithFlags(&ev_h2d_[i], cudaEventDisableTiming));
+            CUDA_CHECK(cudaEventCreateWithFlags(&ev_done_[i], cudaEventDisableTiming));
+            CUDA_CHECK(cudaEventCreateWithFlags(&ev_d2h_[i], cudaEventDisableTiming));
+        }
+    }
+    const int slot = (int)(hseq_ & 1);
+    const size_t fsz = (size_t)c * h * w;
+    ensure_staging(c, h, w, false);
+    if (hframe_d_[slot].n < fsz) {
+        CUDA_CHECK(cudaDeviceSynchronize());
+        hframe_d_[slot].alloc(fsz);
+    }
+    // frame buffer free once the slot's previous frame finished computing
+    CUDA_CHECK(cudaStreamWaitEvent(cstream_, ev_done_[slot], 0));
+    CUDA_CHECK(cudaMemcpyAsync(hframe_d_[slot].p, frame, fsz * 4, cudaMemcpyHostToDevice, cstream_));
+    CUDA_CHECK(cudaEventRecord(ev_h2d_[slot], cstream_));
+    // output buffer free once the slot's previous output copy finished
+    CUDA_CHECK(cudaStreamWaitEvent(stream_, ev_h2d_[slot], 0));
+    CUDA_CHECK(cudaStreamWaitEvent(stream_, ev_d2h_[slot], 0));
+    if (initialized_ && hout_d_[slot].n < out_d_.n) hout_d_[slot].alloc(out_d_.n);
+    out_cur_ = initialized_ ? hout_d_[slot].p : nullptr;
+    enqueue(hframe_d_[slot].p, c, h, w, h9, nullptr);
+    const float* result = out_cur_ ? out_cur_ : out_d_.p;
+    out_cur_ = nullptr;
+    CUDA_CHECK(cudaEventRecord(ev_done_[slot], stream_));
+    const size_t n = (size_t)pending_.out_channels * pending_.out_height * pending_.out_width;
+    CUDA_CHECK(cudaStreamWaitEvent(dstream_, ev_done_[slot], 0));
+    if (out && cap >= n) CUDA_CHECK(cudaMemcpyAsync(out, result, n * 4, cudaMemcpyDeviceToHost, dstream_));
+    CUDA_CHECK(cudaEventRecord(ev_d2h_[slot], dstream_));
+    ++hseq_;
+}
+
 void Engine::sync(dfx_frame_info* info) {
     CUDA_CHECK(cudaSetDevice(device_));
+    if (cstream_) CUDA_CHECK(cudaStreamSynchronize(cstream_));
+    if (dstream_) CUDA_CHECK(cudaStreamSynchronize(dstream_));
     CUDA_CHECK(cudaStreamSynchronize(stream_));
     CUDA_CHECK(cudaGetLastError());
     check(have_frame_, "no frame submitted");
@@ -1144,6 +1226,19 @@ int dfx_engine_run_frame(dfx_engine* e, const float* frame, int c, int h, int w,
 }
 int dfx_engine_submit_frame(dfx_engine* e, const float* frame_dev, int c, int h, int w, const float* h9) {
     return guard([&] { e->e->submit(frame_dev, c, h, w, h9); });
+}
+// Page-locked host memory from this library's CUDA runtime (frames / outputs
+// for dfx_engine_submit_host_frame).
+void* dfx_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    return cudaMallocHost(&p, bytes) == cudaSuccess ? p : nullptr;
+}
+void dfx_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+int dfx_engine_submit_host_frame(dfx_engine* e, const float* frame, int c, int h, int w, const float* h9, float* out,
+                                 size_t out_cap) {
+    return guard([&] { e->e->submit_host(frame, c, h, w, h9, out, out_cap); });
 }
 int dfx_engine_sync(dfx_engine* e, dfx_frame_info* info) {
     return guard([&] { e->e->sync(info); });

@@ -160,6 +160,16 @@ class DeltaEngine:
         _raise(self._api, self._api["submit_frame"](self._h, C.c_void_p(frame_dev_ptr), c, h, w,
                                                     h9.ctypes.data_as(_fp)))
 
+    def submit_host_frame(self, frame_ptr: int, c: int, h: int, w: int, homography, out_ptr: int = 0,
+                          out_floats: int = 0):
+        """Pipelined host-buffer frame (dfx_engine_submit_host_frame): pinned
+        host frame in, densified output copied to `out_ptr` (pinned, CHW)
+        asynchronously; results after sync()."""
+        h9 = np.ascontiguousarray(np.asarray(homography, dtype=np.float32).ravel())
+        _raise(self._api, self._api["submit_host_frame"](self._h, C.c_void_p(frame_ptr), c, h, w,
+                                                         h9.ctypes.data_as(_fp), C.c_void_p(out_ptr or None),
+                                                         out_floats))
+
     def sync(self) -> dict:
         info = FrameInfo()
         _raise(self._api, self._api["sync"](self._h, C.byref(info)))
