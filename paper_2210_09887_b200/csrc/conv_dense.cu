@@ -234,6 +234,7 @@ struct DenseArgs {
     const int* units;
     const int* nunits;
     float* ws;       // split-K partials [S][n*128][cout_pad] (smax > 1)
+    int* cnt;        // split-K arrival counters per (unit group, N-block); self-resetting
     int cin, cout, cout_pad, k, r;
     int KC, nCB, NBD, nNB, nst;
     int smax, sms;
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar_full[8], bar_empty[8], bar_pf[2], bar_pe[2], bar_af[2], bar_ae[2];
     __shared__ uint32_t tmem_base_sh;
+    __shared__ int s_last;
 
     const FrameDev& F = *c.f;
     const int n = *a.nunits;
@@ -565,6 +567,43 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&bar_ae[b]));
+            if (S > 1) {
+                // split-K: the CTA whose partial arrives last sums all S partials of
+                // this (unit group, N-block) in split order (deterministic) into the packet
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (q == 0 && lane == 0) {
+                    __threadfence();
+                    s_last = atomicAdd(a.cnt + it / S, 1) == S - 1;
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (s_last) {
+                    __threadfence();
+                    for (int j = 0; j < nu; ++j) {
+                        const int u = UPI * pr + j;
+                        const int uv = __ldg(a.units + u);
+                        const int y = ((uv >> 16) - 1) * kUY + (m >> 3), x = ((uv & 0xffff) - 1) * kUX + (m & 7);
+                        if (!(y >= -hs && y < eh && x >= -hs && x < ew)) continue;
+                        float* dst = a.out.d + pkt_off(a.out, y, x);
+                        const int o1 = min(a.cout, (nb + 1) * a.NBD);
+                        for (int o = nb * a.NBD; o < o1; o += 4) {
+                            const float* src = a.ws + ((size_t)u * 128 + m) * a.cout_pad + o;
+                            float4 acc4 = __ldcg(reinterpret_cast<const float4*>(src));
+                            for (int sp = 1; sp < S; ++sp) {
+                                const float4 v = __ldcg(reinterpret_cast<const float4*>(src + (size_t)sp * n * 128 * a.cout_pad));
+                                acc4.x = __fadd_rn(acc4.x, v.x), acc4.y = __fadd_rn(acc4.y, v.y);
+                                acc4.z = __fadd_rn(acc4.z, v.z), acc4.w = __fadd_rn(acc4.w, v.w);
+                            }
+                            if ((a.out.C & 3) == 0 && o + 4 <= o1) {
+                                *reinterpret_cast<float4*>(dst + o) = acc4;
+                            } else {
+                                const float vv[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
+                                for (int e = 0; e < 4 && o + e < o1; ++e) dst[o + e] = vv[e];
+                            }
+                        }
+                    }
+                    if (q == 0 && lane == 0) a.cnt[it / S] = 0;
+                }
+            }
             if ((a.dbg & 64) && blockIdx.x == 0 && tid == 128 * kProdWG + 128 && ui < 4) {
                 a.trace[504 + 2 * ui] = t_e0;
                 a.trace[505 + 2 * ui] = clock64();
@@ -796,9 +835,9 @@ static void launch_kc(int grid, size_t smem, cudaStream_t s, const Ctx& c, const
 static long long* g_trace = nullptr;
 long long* dense_conv_trace_buffer() { return g_trace; }
 void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,
-                       int cin, int cout, const int* units, const int* nunits, float* ws, int num_sms) {
+                       int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms) {
     if (!p.ok) throw std::runtime_error("conv_dense: unsupported layer shape");
-    DenseArgs a{in, out, w, units, nunits, p.smax > 1 ? ws : nullptr, cin, cout, p.cout_pad, p.k, p.r,
+    DenseArgs a{in, out, w, units, nunits, p.smax > 1 ? ws : nullptr, cnt, cin, cout, p.cout_pad, p.k, p.r,
                 p.KC, p.nCB, p.NBD, p.nNB, p.nstw, p.smax > 1 ? p.smax : 1, num_sms, p.s_c4, p.patch_bytes,
                 p.w_stage, p.acc_cols, p.nbuf, p.nbuf * p.acc_cols, p.umax, nullptr, 0};
     if (getenv("DFX_CONV_DBG") && !g_trace) cudaMalloc(&g_trace, 1024 * 8);
@@ -815,7 +854,7 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
     if (p.KC == 32) launch_kc<32>(grid, p.smem, s, c, a);
     else if (p.KC == 16) launch_kc<16>(grid, p.smem, s, c, a);
     else launch_kc<8>(grid, p.smem, s, c, a);
-    if (a.smax > 1) launch_pdl(k_conv_dense_reduce, num_sms * 4, 256, 0, s, c, a);
+    // split-K partials are reduced inside k_conv_dense (last-arriving CTA)
 }
 
 }  // namespace dfx

@@ -178,6 +178,7 @@ class Engine {
         bool dense = false;
         DenseConvPlan dp{};
         DevArr<float> wdense, wsd;
+        DevArr<int> dcnt;
         DevArr<int> units;
     };
 
@@ -399,6 +400,8 @@ void Engine::allocate(int th, int tw) {
                         CUDA_CHECK(cudaMemcpy(rt.wdense.p, wd.data(), wd.size() * 4, cudaMemcpyHostToDevice));
                         rt.units.alloc(rt.dp.units_max);
                         if (rt.dp.smax > 1) rt.wsd.alloc((size_t)rt.dp.smax * rt.dp.units_max * 128 * rt.dp.cout_pad);
+                        rt.dcnt.alloc((size_t)rt.dp.units_max * rt.dp.nNB);
+                        CUDA_CHECK(cudaMemset(rt.dcnt.p, 0, rt.dcnt.n * sizeof(int)));
                     }
                 }
                 break;
@@ -693,8 +696,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                     PROF(DFX_FAM_CONV_TARGETS, launch_conv_plan(C, s, rt.dp, a, rt.pkt, rt.halo_geom, rt.units.p,
                                                                 ucounts + idx2, flop_px + idx2));
                     PROF(DFX_FAM_CONV_MMA, launch_conv_dense(C, s, rt.dp, a, rt.pkt, rt.wdense.p, l.cin, l.cout,
-                                                             rt.units.p, ucounts + idx2, rt.wsd.p, num_sms_));
-                    if (rt.dp.smax > 1) ++launches_;
+                                                             rt.units.p, ucounts + idx2, rt.wsd.p, rt.dcnt.p, num_sms_));
                     break;
                 }
                 PROF(DFX_FAM_CONV_TARGETS, launch_conv_targets(C, s, a, l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom, rt.list.p, counts + idx2,
@@ -715,9 +717,9 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
             case DFX_RELU:
             case DFX_TRUNCATE:
             case DFX_OUTPUT:
-                if (a.halo > 0) PROF(DFX_FAM_TRUNC, launch_ring_add(C, s, a, rt.aux));
+                if (a.halo > 0 && (a.C & 3) != 0) PROF(DFX_FAM_TRUNC, launch_ring_add(C, s, a, rt.aux));
                 {
-                    // two streaming passes: tile max, then fire / fold (kernels_hbm.cu)
+                    // two streaming passes: tile max (+ the halo stash), then fire / fold (kernels_hbm.cu)
                     const int pi = prof_begin(DFX_FAM_TRUNC);
                     const bool two = launch_trunc_two_pass(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots,
                                                            rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt);

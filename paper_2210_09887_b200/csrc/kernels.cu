@@ -343,23 +343,32 @@ __global__ void k_input_apply(Ctx c, const float* __restrict__ aligned, const ui
 
 // Claimed tiles of every buffer: zero, or the bias-init fill for truncated
 // buffers (buffer_manager.cpp:68-89, engine.cpp:78-91; fill after zero == fill).
-__global__ void k_claims(Ctx c, const int* __restrict__ claim_slots, const ClaimBuf* __restrict__ bufs) {
+// Persistent grid-stride over (buffer, claim, element) with 16-byte stores.
+__global__ void k_claims(Ctx c, const int* __restrict__ claim_slots, const ClaimBuf* __restrict__ bufs, int nbuf) {
     pdl_enter();
     const FrameDev& F = *c.f;
-    const int ci = blockIdx.x;
-    if (ci >= F.nclaims) return;
-    const ClaimBuf b = bufs[blockIdx.y];
-    const size_t n = (size_t)b.t * b.t * b.C;
-    float* dst = b.d + (size_t)claim_slots[ci] * n;
-    if (!b.fill) {
-        float4* d4 = reinterpret_cast<float4*>(dst);
-        if ((n & 3) == 0) {
-            for (size_t i = threadIdx.x; i < n / 4; i += blockDim.x) d4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int nq = F.nclaims;
+    const long long tid0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, nthr = (long long)gridDim.x * blockDim.x;
+    for (int bi = 0; bi < nbuf; ++bi) {
+        const ClaimBuf b = bufs[bi];
+        const long long n = (long long)b.t * b.t * b.C;  // floats per tile
+        if ((b.C & 3) == 0) {
+            const long long n4 = n / 4;
+            for (long long e = tid0; e < (long long)nq * n4; e += nthr) {
+                const long long ci = e / n4, r = e - ci * n4;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (b.fill) {
+                    const int ch = (int)((r * 4) % b.C);
+                    v = make_float4(b.fill[ch], b.fill[ch + 1], b.fill[ch + 2], b.fill[ch + 3]);
+                }
+                reinterpret_cast<float4*>(b.d + (size_t)claim_slots[ci] * n)[r] = v;
+            }
         } else {
-            for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = 0.0f;
+            for (long long e = tid0; e < (long long)nq * n; e += nthr) {
+                const long long ci = e / n, r = e - ci * n;
+                b.d[(size_t)claim_slots[ci] * n + r] = b.fill ? b.fill[r % b.C] : 0.0f;
+            }
         }
-    } else {
-        for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = b.fill[i % b.C];
     }
 }
 
@@ -1139,7 +1148,7 @@ void launch_input_apply(const Ctx& c, cudaStream_t s, const float* aligned, cons
 void launch_claims(const Ctx& c, cudaStream_t s, const int* claim_slots, const ClaimBuf* bufs, int nbuf,
                    int max_claims) {
     if (nbuf <= 0 || max_claims <= 0) return;
-    launch_pdl(k_claims, dim3(max_claims, nbuf), kThreads, 0, s, c, claim_slots, bufs);
+    launch_pdl(k_claims, num_sms_cached() * 8, kThreads, 0, s, c, claim_slots, bufs, nbuf);
 }
 void launch_ring_add(const Ctx& c, cudaStream_t s, PktDev in, BufDev dst) {
     if (in.halo <= 0) return;

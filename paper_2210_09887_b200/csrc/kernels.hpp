@@ -107,7 +107,7 @@ void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktD
                       int* nunits, unsigned long long* flop_px);
 long long* dense_conv_trace_buffer();  // microbenchmark stamps (DFX_CONV_DBG & 64)
 void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,
-                       int cin, int cout, const int* units, const int* nunits, float* ws, int num_sms);
+                       int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms);
 
 // ---- output (delta_layers.cpp:395-400) ----
 void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out);

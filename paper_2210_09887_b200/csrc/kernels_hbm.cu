@@ -27,15 +27,58 @@ namespace {
 constexpr int kSub = 8;               // float4s per lane in flight per array
 constexpr int kChunkF4 = 32 * kSub;   // float4s per warp work item (4 KB): one round, all loads issued up front
 
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+    return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
 // Placement tile (qy, qx) owns its slot (TileLedger::holds, buffer_manager.hpp:41-44).
 __device__ __forceinline__ bool holds_t(const Ctx& c, const FrameDev& F, int qy, int qx) {
     return c.own[qy * F.tw + qx] != 0;
 }
+// Any tile, ring tiles outside the placement included (slot table).
+__device__ __forceinline__ bool holds_any(const Ctx& c, const FrameDev& F, int qy, int qx) {
+    if (qy >= 0 && qy < F.th && qx >= 0 && qx < F.tw) return c.own[qy * F.tw + qx] != 0;
+    const SlotDev& sl = c.slots[slot_of(F, c.rows, c.cols, qy, qx)];
+    return sl.used && sl.ty == F.oty + qy && sl.tx == F.otx + qx;
+}
+
+// Halo stash (delta_layers.cpp:168-183; maxpool acc :262-275): every written
+// ring pixel of the grown packet is added into the wrapped buffer when its
+// slot is owned. Ring pixels map to distinct buffer pixels, so this is a plain
+// vectorised read-modify-write (no atomics, deterministic). Spread over all
+// threads of the grid (tid0 / nthr).
+__device__ void ring_add_part(const Ctx& c, const FrameDev& F, const PktDev& in, BufDev dst, long long tid0,
+                              long long nthr) {
+    const int h = in.halo, t = in.t, C4 = in.C / 4;
+    if (h <= 0) return;
+    const int eh = F.th * t, ew = F.tw * t, gw = ew + 2 * h;
+    const long long npx = 2LL * h * gw + 2LL * eh * h;
+    for (long long i = tid0; i < npx * C4; i += nthr) {
+        const long long p = i / C4;
+        const int c4 = (int)(i - p * C4);
+        int y, x;
+        if (p < (long long)h * gw) {
+            y = -h + (int)(p / gw), x = -h + (int)(p % gw);
+        } else if (p < 2LL * h * gw) {
+            const long long q = p - (long long)h * gw;
+            y = eh + (int)(q / gw), x = -h + (int)(q % gw);
+        } else if (p < 2LL * h * gw + (long long)eh * h) {
+            const long long q = p - 2LL * h * gw;
+            y = (int)(q / h), x = -h + (int)(q % h);
+        } else {
+            const long long q = p - 2LL * h * gw - (long long)eh * h;
+            y = (int)(q / h), x = ew + (int)(q % h);
+        }
+        const int qy = floor_div32(y, t), qx = floor_div32(x, t);
+        if (!in.ext[ext_idx(in, qy, qx)] || !holds_any(c, F, qy, qx)) continue;
+        float4* b = reinterpret_cast<float4*>(
+                        dst.d + (size_t)slot_of(F, c.rows, c.cols, qy, qx) * dst.t * dst.t * dst.C +
+                        ((size_t)(y - qy * t) * t + (x - qx * t)) * dst.C) + c4;
+        const float4 dv = reinterpret_cast<const float4*>(in.d + pkt_off(in, y, x))[c4];
+        *b = add4(*b, dv);
+    }
+}
 __device__ __forceinline__ float* tile_base(const Ctx& c, const FrameDev& F, BufDev b, int qy, int qx) {
     return b.d + (size_t)slot_of(F, c.rows, c.cols, qy, qx) * b.t * b.t * b.C;
-}
-__device__ __forceinline__ float4 add4(float4 a, float4 b) {
-    return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
 }
 __device__ __forceinline__ float amax4(float m, float4 v) {
     return fmaxf(fmaxf(fmaxf(m, fabsf(v.x)), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
@@ -91,6 +134,8 @@ __device__ __forceinline__ const float4* pkt_f4(const PktDev& p, int tr, int tc,
 
 __global__ void __launch_bounds__(256) k_trunc_tilemax(Ctx c, PktDev in, BufDev trunc, unsigned* __restrict__ tile_max) {
     pdl_enter();
+    // the halo stash touches ring slots only (never this frame's placement tiles): independent work
+    ring_add_part(c, *c.f, in, trunc, blockIdx.x * (long long)blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
     __shared__ int s_list[kMaxList];
     __shared__ int s_warp[8];
     const FrameDev& F = *c.f;

@@ -76,6 +76,9 @@ int main(int argc, char** argv) {
         CK(cudaMemcpy(dw, wd.data(), wd.size() * 4, cudaMemcpyHostToDevice));
         float* ws = nullptr;
         if (p.smax > 1) CK(cudaMalloc(&ws, (size_t)p.smax * p.units_max * 128 * p.cout_pad * 4));
+        int* dcnt;
+        CK(cudaMalloc(&dcnt, (size_t)p.units_max * p.nNB * 4));
+        CK(cudaMemset(dcnt, 0, (size_t)p.units_max * p.nNB * 4));
         const int eh = th * g.t;
         const int nuy = eh / 16, nux = eh / 8;
         std::vector<int> units;
@@ -121,9 +124,9 @@ int main(int argc, char** argv) {
             float ms_d = 0, ms_g = 0;
             const int it = 10;
             for (int rep = 0; rep < 2; ++rep) {
-                for (int i = 0; i < 2; ++i) launch_conv_dense(c, s, p, in, out, dw, g.cin, g.cout, du, dn, ws, sms);
+                for (int i = 0; i < 2; ++i) launch_conv_dense(c, s, p, in, out, dw, g.cin, g.cout, du, dn, ws, dcnt, sms);
                 CK(cudaEventRecord(a, s));
-                for (int i = 0; i < it; ++i) launch_conv_dense(c, s, p, in, out, dw, g.cin, g.cout, du, dn, ws, sms);
+                for (int i = 0; i < it; ++i) launch_conv_dense(c, s, p, in, out, dw, g.cin, g.cout, du, dn, ws, dcnt, sms);
                 CK(cudaEventRecord(b, s));
                 CK(cudaEventSynchronize(b));
                 CK(cudaEventElapsedTime(&ms_d, a, b));
@@ -141,7 +144,7 @@ int main(int argc, char** argv) {
             CK(cudaGetLastError());
             if (dbg && (atoi(dbg) & 64)) {
                 // one more launch, then dump CTA 0's per-K-block stamps
-                launch_conv_dense(c, s, p, in, out, dw, g.cin, g.cout, du, dn, ws, sms);
+                launch_conv_dense(c, s, p, in, out, dw, g.cin, g.cout, du, dn, ws, dcnt, sms);
                 CK(cudaStreamSynchronize(s));
                 long long tr[1024];
                 CK(cudaMemcpy(tr, dense_conv_trace_buffer(), sizeof tr, cudaMemcpyDeviceToHost));
