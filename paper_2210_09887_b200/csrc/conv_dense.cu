@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
     __shared__ uint32_t s_bits[4096 / 32];
     __shared__ int s_ucnt[32];
     __shared__ int s_tstore[32];
+    __shared__ int s_geo[kPlanThreads / 32];
     const FrameDev& F = *c.f;
     const int t = out.t;
     const int BH = t > kUY ? t : kUY, BW = t > kUX ? t : kUX;
@@ -185,22 +186,31 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
     for (int p0 = 0; p0 < npx; p0 += kPlanThreads) {
         const int p = p0 + threadIdx.x;
         bool tgt = false;
+        int uid = -1;
         if (p < npx) {
             const int ly = p / BW, lx = p - (p / BW) * BW;
             const int y = Y0 + ly, x = X0 + lx;
             if (y >= -hg && y < eh + hg && x >= -hg && x < ew + hg) tgt = is_target_s1(in, F.th, F.tw, y, x, k, r);
             if (tgt) {
                 ++geo;
-                atomicAdd(&s_ucnt[(ly / kUY) * upr + lx / kUX], 1);
+                uid = (ly / kUY) * upr + lx / kUX;
                 if (y >= -hs && y < eh + hs && x >= -hs && x < ew + hs) s_tstore[(ly / t) * tpr + lx / t] = 1;
             }
         }
+        // per-unit target counts, aggregated per warp (one shared atomic per unit and warp)
+        const unsigned grp = __match_any_sync(0xffffffffu, uid);
+        if (uid >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&s_ucnt[uid], __popc(grp));
         const unsigned m = __ballot_sync(0xffffffffu, tgt);
         if ((threadIdx.x & 31) == 0 && p < npx) s_bits[p >> 5] = m;
     }
     for (int o = 16; o > 0; o >>= 1) geo += __shfl_xor_sync(0xffffffffu, geo, o);
-    if ((threadIdx.x & 31) == 0 && geo) atomicAdd(flop_px, (unsigned long long)geo);
+    if ((threadIdx.x & 31) == 0) s_geo[threadIdx.x >> 5] = geo;
     __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < kPlanThreads / 32; ++w) tot += s_geo[w];
+        if (tot) atomicAdd(flop_px, (unsigned long long)tot);  // one global atomic per block
+    }
     if (threadIdx.x < nun && s_ucnt[threadIdx.x] > 0) {
         const int uy = Y0 / kUY + threadIdx.x / upr, ux = X0 / kUX + threadIdx.x % upr;
         units[atomicAdd(nunits, 1)] = ((uy + 1) << 16) | (ux + 1);
@@ -211,7 +221,9 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
             out.ext[ext_idx(out, ti, tj)] = s_tstore[threadIdx.x] ? 1 : 0;
     }
     // zero fill: stored pixels of active tiles in units without targets
-    if (nun > 1) {
+    const bool empty_unit = __syncthreads_or(threadIdx.x < nun && s_ucnt[threadIdx.x] == 0);
+    const bool active_tile = __syncthreads_or(threadIdx.x < ntl && s_tstore[threadIdx.x]);
+    if (nun > 1 && empty_unit && active_tile) {
         const int C = out.C;
         for (int e = threadIdx.x; e < npx * ((C & 3) == 0 ? C / 4 : C); e += kPlanThreads) {
             const int per = (C & 3) == 0 ? C / 4 : C;
