@@ -196,6 +196,9 @@ int dfx_engine_read_packet(dfx_engine* e, const char* layer, float* out, size_t 
 int dfx_engine_read_ledger(dfx_engine* e, int* used, int64_t* ty, int64_t* tx, uint8_t* covered,
                            size_t cap);
 
+/* Debug: per-layer gathered conv targets and dense 16x8 units of the last frame. */
+int dfx_engine_debug_counts(dfx_engine* e, int* gathered, int* units, int cap);
+
 /* Number of kernels the last frame launched. */
 int dfx_engine_kernel_count(dfx_engine* e);
 

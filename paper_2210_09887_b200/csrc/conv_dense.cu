@@ -159,7 +159,8 @@ constexpr int kPlanThreads = 256;
 __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, PktDev out, int k, int r, int hg,
                                                             int nbw, int* __restrict__ units,
                                                             int* __restrict__ nunits,
-                                                            unsigned long long* __restrict__ flop_px) {
+                                                            unsigned long long* __restrict__ flop_px, int tau,
+                                                            int* __restrict__ list, int* __restrict__ lcount) {
     pdl_enter();
     __shared__ uint32_t s_bits[4096 / 32];
     __shared__ int s_ucnt[32];
@@ -211,25 +212,46 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
         for (int w = 0; w < kPlanThreads / 32; ++w) tot += s_geo[w];
         if (tot) atomicAdd(flop_px, (unsigned long long)tot);  // one global atomic per block
     }
-    if (threadIdx.x < nun && s_ucnt[threadIdx.x] > 0) {
+    // units with >= tau targets are computed whole by k_conv_dense
+    if (threadIdx.x < nun && s_ucnt[threadIdx.x] >= tau) {
         const int uy = Y0 / kUY + threadIdx.x / upr, ux = X0 / kUX + threadIdx.x % upr;
         units[atomicAdd(nunits, 1)] = ((uy + 1) << 16) | (ux + 1);
+    }
+    // targets of sparser units go to the gathered kernel (stored extent only)
+    if (tau > 1) {
+        for (int p0 = 0; p0 < npx; p0 += kPlanThreads) {
+            const int p = p0 + threadIdx.x;
+            bool g = false;
+            int y = 0, x = 0;
+            if (p < npx && ((s_bits[p >> 5] >> (p & 31)) & 1u)) {
+                const int ly = p / BW, lx = p - (p / BW) * BW;
+                y = Y0 + ly, x = X0 + lx;
+                g = s_ucnt[(ly / kUY) * upr + lx / kUX] < tau && y >= -hs && y < eh + hs && x >= -hs && x < ew + hs;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, g);
+            int base = 0;
+            if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(lcount, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (g) list[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = ((y + hg) << 16) | (x + hg);
+        }
     }
     if (threadIdx.x < ntl) {
         const int ti = floor_div32(Y0, t) + threadIdx.x / tpr, tj = floor_div32(X0, t) + threadIdx.x % tpr;
         if (ti >= -out.RT && ti < F.th + out.RT && tj >= -out.RT && tj < F.tw + out.RT)
             out.ext[ext_idx(out, ti, tj)] = s_tstore[threadIdx.x] ? 1 : 0;
     }
-    // zero fill: stored pixels of active tiles in units without targets
-    const bool empty_unit = __syncthreads_or(threadIdx.x < nun && s_ucnt[threadIdx.x] == 0);
+    // zero fill: non-target stored pixels of active tiles outside dense units
+    const bool sparse_unit = __syncthreads_or(threadIdx.x < nun && s_ucnt[threadIdx.x] < tau);
     const bool active_tile = __syncthreads_or(threadIdx.x < ntl && s_tstore[threadIdx.x]);
-    if (nun > 1 && empty_unit && active_tile) {
+    if ((nun > 1 || tau > 1) && sparse_unit && active_tile) {
         const int C = out.C;
         for (int e = threadIdx.x; e < npx * ((C & 3) == 0 ? C / 4 : C); e += kPlanThreads) {
             const int per = (C & 3) == 0 ? C / 4 : C;
             const int p = e / per, q = e - p * per;
             const int ly = p / BW, lx = p - (p / BW) * BW;
-            if (s_ucnt[(ly / kUY) * upr + lx / kUX] > 0 || !s_tstore[(ly / t) * tpr + lx / t]) continue;
+            if (s_ucnt[(ly / kUY) * upr + lx / kUX] >= tau || !s_tstore[(ly / t) * tpr + lx / t] ||
+                ((s_bits[p >> 5] >> (p & 31)) & 1u))
+                continue;
             const int y = Y0 + ly, x = X0 + lx;
             if (y < -hs || y >= eh + hs || x < -hs || x >= ew + hs) continue;
             if ((C & 3) == 0)
@@ -274,14 +296,12 @@ struct DenseSched {
 // else one; split-K only when even single-unit items leave most SMs idle
 // (partials cost a workspace round trip).
 __host__ __device__ __forceinline__ DenseSched dense_sched(int n, int nNB, int nKB, int smax, int sms, int umax) {
-    DenseSched d{1, 1, n * nNB};
-    if (umax >= 2 && (long long)((n + 1) / 2) * nNB >= sms) {
-        d.U = 2;
-        d.items = ((n + 1) / 2) * nNB;
-        return d;
-    }
-    while (d.S * 2 <= smax && (long long)n * nNB * d.S * 2 <= sms && nKB / (d.S * 2) >= 4) d.S *= 2;
-    d.items = n * nNB * d.S;
+    // two units per item whenever the plan allows it (weight streaming from L2
+    // is the limit: it halves the bytes per FLOP); split-K fills idle SMs
+    DenseSched d{umax >= 2 ? 2 : 1, 1, 0};
+    const int groups = (n + d.U - 1) / d.U;
+    while (d.S * 2 <= smax && (long long)groups * nNB * d.S * 2 <= sms && nKB / (d.S * 2) >= 4) d.S *= 2;
+    d.items = groups * nNB * d.S;
     return d;
 }
 
@@ -348,6 +368,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     __shared__ __align__(8) uint64_t bar_full[8], bar_empty[8], bar_pf[2], bar_pe[2], bar_af[2], bar_ae[2];
     __shared__ uint32_t tmem_base_sh;
     __shared__ int s_last;
+    __shared__ int s_poff[2 * 22 * 14];  // per-pixel patch source offsets (k <= 7, two units)
 
     const FrameDev& F = *c.f;
     const int n = *a.nunits;
@@ -477,6 +498,17 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                 x0[j] = ((uv & 0xffff) - 1) * kUX - a.r;
             }
             const int E = E1 * nu;
+            // per-pixel source offset (-1: zero) of the item's patches, once per item:
+            // keeps the dependent ext-map lookups out of the per-chunk copy loop
+            const int P = PW * (kUY + 2 * a.r);
+            asm volatile("bar.sync 2, 128;" ::: "memory");  // previous item's copy loop is done with s_poff
+            for (int q = lt; q < P * nu; q += 128) {
+                const int j = q >= P ? 1 : 0, p = q - j * P;
+                const int py = p / PW, px = p - py * PW;
+                const int y = (j ? y0[1] : y0[0]) + py, x = (j ? x0[1] : x0[0]) + px;
+                s_poff[q] = pkt_ok(a.in, F.th, F.tw, y, x) ? (int)pkt_off(a.in, y, x) : -1;
+            }
+            asm volatile("bar.sync 2, 128;" ::: "memory");
             for (int cb = kb0 / K2; cb <= (kb1 - 1) / K2; ++cb, ++pseq) {
                 const int pb = pseq & 1;
                 mbar_wait(smem_u32(&bar_pe[pb]), ((pseq >> 1) & 1) ^ 1);
@@ -486,16 +518,15 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                     const int j = e >= E1 ? 1 : 0;
                     const int e1 = e - j * E1;
                     const int p = e1 / c4n, c4 = e1 - p * c4n;
-                    const int py = p / PW, px = p - py * PW;
-                    const int y = (j ? y0[1] : y0[0]) + py, x = (j ? x0[1] : x0[0]) + px;
                     const int ch = cbase + c4 * 4;
                     const uint32_t dst = buf + j * unit_bytes + p * a.pstr + c4 * 16;
-                    const bool ok = pkt_ok(a.in, F.th, F.tw, y, x);
+                    const int off = s_poff[j * P + p];
+                    const bool ok = off >= 0;
                     if (vec) {
                         const bool v = ok && ch < a.cin;
-                        cp_async16(dst, v ? a.in.d + pkt_off(a.in, y, x) + ch : a.in.d, v ? 16u : 0u);
+                        cp_async16(dst, v ? a.in.d + off + ch : a.in.d, v ? 16u : 0u);
                     } else {
-                        const float* src = ok ? a.in.d + pkt_off(a.in, y, x) : a.in.d;
+                        const float* src = ok ? a.in.d + off : a.in.d;
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
                             const bool v = ok && ch + q < a.cin;
@@ -755,8 +786,14 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     // One unit per item (measured best on the C2 layers: more SMs busy, and
     // 32-channel K-blocks amortise the per-K-block handshake); the kernel also
     // supports two units sharing each weight stage (umax = 2).
-    p.umax = 1;
-    p.KC = p.cin_pad % 32 == 0 ? 32 : (p.cin_pad % 16 == 0 ? 16 : 8);
+    // two units per weight stage (16-channel K-blocks keep accumulators + A
+    // stages within TMEM) halve the weight stream; one unit per item keeps more
+    // SMs busy and amortises the per-K-block handshake over 32 channels
+    const long long wbytes = (long long)cin * cout * k * k * 8;
+    p.umax = 1;  // measured: one unit per item wins on the C2 layers (DFX_DENSE_UMAX=2 to compare)
+    (void)wbytes;
+    if (const char* u = getenv("DFX_DENSE_UMAX")) p.umax = atoi(u) >= 2 ? 2 : 1;
+    p.KC = p.umax == 2 ? 16 : (p.cin_pad % 32 == 0 ? 32 : (p.cin_pad % 16 == 0 ? 16 : 8));
     p.nCB = p.cin_pad / p.KC;
     p.r = k / 2;
     p.k = k;
@@ -829,9 +866,10 @@ void dense_conv_prepare_weights(const DenseConvPlan& p, const float* w, int cin,
 }
 
 void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, int hg, int* units,
-                      int* nunits, unsigned long long* flop_px) {
+                      int* nunits, unsigned long long* flop_px, int tau, int* list, int* lcount) {
     if (hg > 8) throw std::runtime_error("conv_plan: grown halo > 8 px");
-    launch_pdl(k_conv_plan, p.nbh * p.nbw, kPlanThreads, 0, s, c, in, out, p.k, p.r, hg, p.nbw, units, nunits, flop_px);
+    launch_pdl(k_conv_plan, p.nbh * p.nbw, kPlanThreads, 0, s, c, in, out, p.k, p.r, hg, p.nbw, units, nunits, flop_px,
+               tau, list, lcount);
 }
 
 template <int KC>

@@ -149,6 +149,13 @@ class Engine {
     int cols() const { return cols_; }
     int num_layers() const { return (int)net_.layers.size(); }
     int kernel_count() const { return launches_; }
+    void debug_counts(int* g, int* u, int cap) {
+        CUDA_CHECK(cudaStreamSynchronize(stream_));
+        const int nl = (int)net_.layers.size();
+        std::vector<int> h(2 * nl);
+        CUDA_CHECK(cudaMemcpy(h.data(), counters_d_.p + off_counts_, 2 * nl * sizeof(int), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < nl && i < cap; ++i) g[i] = h[i], u[i] = h[nl + i];
+    }
     void set_profiling(bool on);
     void profile(int fam, double* ms, uint64_t* launches, double* work) const;
     void reset_profile();
@@ -692,9 +699,18 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
         switch (l.kind) {
             case DFX_CONV:
                 if (rt.dense) {
-                    // every target of a stride-1 conv is computed by dense units
+                    // stride-1 conv: 16x8-pixel units with >= tau targets computed whole
+                    // (k_conv_dense); at tiles >= 16 px the 1-px ring strips of sparser
+                    // units go to the gathered kernel instead of wasting whole units
+                    const int tau = l.tile >= 16 ? 48 : 1;
                     PROF(DFX_FAM_CONV_TARGETS, launch_conv_plan(C, s, rt.dp, a, rt.pkt, rt.halo_geom, rt.units.p,
-                                                                ucounts + idx2, flop_px + idx2));
+                                                                ucounts + idx2, flop_px + idx2, tau, rt.list.p,
+                                                                counts + idx2));
+                    if (tau > 1)
+                        PROF(DFX_FAM_CONV_MMA, launch_conv_tc(C, s, a, rt.wtc.p, l.cin, rt.cin_pad, l.cout, rt.cout_pad,
+                                                              l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom, rt.list.p,
+                                                              counts + idx2, rt.max_targets, num_sms_, rt.ws.p,
+                                                              rt.splits));
                     PROF(DFX_FAM_CONV_MMA, launch_conv_dense(C, s, rt.dp, a, rt.pkt, rt.wdense.p, l.cin, l.cout,
                                                              rt.units.p, ucounts + idx2, rt.wsd.p, rt.dcnt.p, num_sms_));
                     break;
@@ -1273,6 +1289,20 @@ int dfx_engine_read_packet(dfx_engine* e, const char* layer, float* out, size_t 
 }
 int dfx_engine_read_ledger(dfx_engine* e, int* used, int64_t* ty, int64_t* tx, uint8_t* covered, size_t cap) {
     return guard([&] { e->e->read_ledger(used, ty, tx, covered, cap); });
+}
+// Debug: clock64 stamps of the last dense conv launch (DFX_CONV_DBG & 64).
+int dfx_debug_conv_trace(long long* out, int n) {
+    return guard([&] {
+        long long* t = dfx::dense_conv_trace_buffer();
+        dfx::check(t != nullptr, "no trace (set DFX_CONV_DBG=64)");
+        cudaDeviceSynchronize();
+        dfx::check(cudaMemcpy(out, t, (size_t)(n < 1024 ? n : 1024) * 8, cudaMemcpyDeviceToHost) == cudaSuccess,
+                   "trace copy failed");
+    });
+}
+// Debug: per-layer gathered-target counts and dense-unit counts of the last frame.
+int dfx_engine_debug_counts(dfx_engine* e, int* gathered, int* units, int cap) {
+    return guard([&] { e->e->debug_counts(gathered, units, cap); });
 }
 int dfx_engine_kernel_count(dfx_engine* e) { return e->e->kernel_count(); }
 int dfx_engine_set_profiling(dfx_engine* e, int on) {

@@ -103,8 +103,10 @@ size_t dense_conv_weight_floats(const DenseConvPlan& p);
 void dense_conv_prepare_weights(const DenseConvPlan& p, const float* w, int cin, int cout, float* out);
 // Targets, exact out ext map, FLOP pixels, dense unit list and zero fill of a
 // stride-1 conv whose every target is computed by k_conv_dense.
+// Units with >= tau targets go to k_conv_dense, the targets of sparser units
+// to the gathered list (list / lcount) for launch_conv_tc (tau = 1: all dense).
 void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, int hg, int* units,
-                      int* nunits, unsigned long long* flop_px);
+                      int* nunits, unsigned long long* flop_px, int tau, int* list, int* lcount);
 long long* dense_conv_trace_buffer();  // microbenchmark stamps (DFX_CONV_DBG & 64)
 void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,
                        int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms);
