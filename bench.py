@@ -260,11 +260,14 @@ def run_ours(args):
         ctypes.memmove(p, np.ascontiguousarray(f).ctypes.data, fbytes)
         hframes.append(p)
     eng2 = dfx.DeltaEngine(spec, econf, device=local)
-    for k in range(W):
-        eng2.run_frame_full(seq[k][0], seq[k][1])
+    eng2.run_frame_full(seq[0][0], seq[0][1])
     oc, oh, ow = eng2.last_info["out_channels"], eng2.last_info["out_height"], eng2.last_info["out_width"]
     ocap = oc * (oh + 64) * (ow + 64)
     houts = [capi["host_alloc"](ocap * 4) for _ in range(2)]
+    # warm-up through the same pipelined path (allocates its double buffers outside the timed region)
+    for k in range(1, W):
+        eng2.submit_host_frame(hframes[k], *seq[k][0].shape, seq[k][1], houts[k & 1], ocap)
+    eng2.sync()
     if dist:
         dist.barrier()
     eng2.timer_start()

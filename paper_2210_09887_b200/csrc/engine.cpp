@@ -235,7 +235,7 @@ class Engine {
     int nclaim_bufs_ = 0;
     // per-frame counters: [nl u64 flop_px][u64 dropped][nl int counts][nl * slots u32 tile_max]
     DevArr<uint8_t> counters_d_;
-    size_t cnt_bytes_ = 0, off_dropped_ = 0, off_counts_ = 0, off_ucounts_ = 0, off_tmax_ = 0;
+    size_t cnt_bytes_ = 0, off_dropped_ = 0, off_counts_ = 0, off_ucounts_ = 0, off_gbar_ = 0, off_tmax_ = 0;
     uint8_t* readback_h_ = nullptr;  // pinned: flop_px, dropped, input mask
     float *in_h_ = nullptr, *out_h_ = nullptr;  // pinned staging of run_frame's caller buffers
     size_t in_h_n_ = 0, out_h_n_ = 0;
@@ -506,7 +506,8 @@ void Engine::allocate(int th, int tw) {
     off_dropped_ = nl * 8;
     off_counts_ = off_dropped_ + 8;
     off_ucounts_ = off_counts_ + nl * 4;
-    off_tmax_ = (off_ucounts_ + nl * 4 + 15) / 16 * 16;
+    off_gbar_ = off_ucounts_ + nl * 4;
+    off_tmax_ = (off_gbar_ + nl * 4 + 15) / 16 * 16;
     cnt_bytes_ = off_tmax_ + nl * (size_t)slots * 4;
     counters_d_.alloc(cnt_bytes_);
     CUDA_CHECK(cudaMallocHost(&readback_h_, nl * 8 + 8 + slots));
@@ -662,6 +663,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     auto* dropped = reinterpret_cast<unsigned long long*>(counters_d_.p + off_dropped_);
     int* counts = reinterpret_cast<int*>(counters_d_.p + off_counts_);
     int* ucounts = reinterpret_cast<int*>(counters_d_.p + off_ucounts_);
+    unsigned* gbars = reinterpret_cast<unsigned*>(counters_d_.p + off_gbar_);
     unsigned* tmax = reinterpret_cast<unsigned*>(counters_d_.p + off_tmax_);
     const int nslots = rows_ * cols_;
 
@@ -738,10 +740,10 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                     // two streaming passes: tile max (+ the halo stash), then fire / fold (kernels_hbm.cu)
                     const int pi = prof_begin(DFX_FAM_TRUNC);
                     const bool two = launch_trunc_two_pass(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots,
-                                                           rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt);
+                                                           rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt, gbars + idx2);
                     prof_end(pi);
                     if (two) {
-                        launches_ += 2;
+                        launches_ += 1;
                     } else {
                         PROF(DFX_FAM_TRUNC, launch_trunc_max(C, s, a, rt.aux, tmax + (size_t)idx2 * nslots));
                         PROF(DFX_FAM_TRUNC, launch_trunc_apply(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots,

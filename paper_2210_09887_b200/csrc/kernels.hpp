@@ -50,8 +50,9 @@ void launch_trunc_max(const Ctx& c, cudaStream_t s, PktDev in, BufDev trunc, uns
 bool launch_trunc_fused(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, float thr, int relu,
                         PktDev out);
 // Two streaming passes (kernels_hbm.cu): tile max, then fire / fold. Needs C % 4 == 0.
+// gbar (zeroed per frame): grid-barrier counter for the single cooperative launch.
 bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
-                           float thr, int relu, PktDev out);
+                           float thr, int relu, PktDev out, unsigned* gbar);
 bool launch_maxpool_vec(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, PktDev out);
 void launch_trunc_apply(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
                         const unsigned* tile_max, float thr, int relu, PktDev out);

@@ -16,6 +16,7 @@
 // far smaller than the 126 MB L2), so DRAM sees the algorithmic traffic.
 // Arithmetic is the reference's fp32 order with explicit rounding intrinsics.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "kernels.hpp"
 #include "pdl.hpp"
@@ -132,16 +133,11 @@ __device__ __forceinline__ const float4* pkt_f4(const PktDev& p, int tr, int tc,
     return reinterpret_cast<const float4*>(p.d + pkt_off(p, tr * p.t + yy, tc * p.t)) + rem;
 }
 
-__global__ void __launch_bounds__(256) k_trunc_tilemax(Ctx c, PktDev in, BufDev trunc, unsigned* __restrict__ tile_max) {
-    pdl_enter();
-    // the halo stash touches ring slots only (never this frame's placement tiles): independent work
-    ring_add_part(c, *c.f, in, trunc, blockIdx.x * (long long)blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
-    __shared__ int s_list[kMaxList];
-    __shared__ int s_warp[8];
-    const FrameDev& F = *c.f;
+// Pass 1 of the truncation: max |trunc + delta| per masked owned tile.
+__device__ void tilemax_body(const Ctx& c, const FrameDev& F, const PktDev& in, BufDev trunc,
+                             unsigned* __restrict__ tile_max, const int* s_list, int nl) {
     const int T = in.t, E4 = T * T * in.C / 4, row4 = T * in.C / 4;
     const int nch = (E4 + kChunkF4 - 1) / kChunkF4;
-    const int nl = build_tile_list(c, F, in, true, s_list, s_warp);
     const int items = (nl < 0 ? F.th * F.tw : nl) * nch;
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -172,23 +168,30 @@ __global__ void __launch_bounds__(256) k_trunc_tilemax(Ctx c, PktDev in, BufDev 
     }
 }
 
-__global__ void __launch_bounds__(256) k_trunc_commit(Ctx c, PktDev in, BufDev acc, BufDev trunc,
-                                                      const unsigned* __restrict__ tile_max, float thr, int relu,
-                                                      PktDev out) {
+__global__ void __launch_bounds__(256) k_trunc_tilemax(Ctx c, PktDev in, BufDev trunc, unsigned* __restrict__ tile_max) {
     pdl_enter();
     __shared__ int s_list[kMaxList];
     __shared__ int s_warp[8];
     const FrameDev& F = *c.f;
+    // the halo stash touches ring slots only (never this frame's placement tiles): independent work
+    ring_add_part(c, F, in, trunc, blockIdx.x * (long long)blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
+    const int nl = build_tile_list(c, F, in, true, s_list, s_warp);
+    tilemax_body(c, F, in, trunc, tile_max, s_list, nl);
+}
+
+// Pass 2: output mask of every placement tile, then fire / fold of the masked ones.
+__device__ void commit_body(const Ctx& c, const FrameDev& F, const PktDev& in, BufDev acc, BufDev trunc,
+                            const unsigned* __restrict__ tile_max, float thr, int relu, const PktDev& out,
+                            const int* s_list, int nl) {
     const int T = in.t, E4 = T * T * in.C / 4, row4 = T * in.C / 4;
     const int nch = (E4 + kChunkF4 - 1) / kChunkF4;
     // output mask = fired tiles (delta_layers.cpp:203-204), every placement tile
     for (int ti = blockIdx.x * blockDim.x + threadIdx.x; ti < F.th * F.tw; ti += gridDim.x * blockDim.x) {
         const int tr = ti / F.tw, tc = ti - tr * F.tw;
-        const float tm = __uint_as_float(tile_max[ti]);
+        const float tm = __uint_as_float(__ldcg(tile_max + ti));
         out.ext[ext_idx(out, tr, tc)] =
             (in.ext[ext_idx(in, tr, tc)] && holds_t(c, F, tr, tc) && tm >= thr && tm > 0.0f) ? 1 : 0;
     }
-    const int nl = build_tile_list(c, F, in, true, s_list, s_warp);
     const int items = (nl < 0 ? F.th * F.tw : nl) * nch;
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(256) k_trunc_commit(Ctx c, PktDev in, BufDev a
         const int ti = nl < 0 ? li : s_list[li];
         const int tr = ti / F.tw, tc = ti - tr * F.tw;
         if (nl < 0 && (!in.ext[ext_idx(in, tr, tc)] || !holds_t(c, F, tr, tc))) continue;
-        const float tm = __uint_as_float(tile_max[ti]);
+        const float tm = __uint_as_float(__ldcg(tile_max + ti));
         const bool fire = tm >= thr && tm > 0.0f;
         float4* tb = reinterpret_cast<float4*>(tile_base(c, F, trunc, tr, tc));
         float4* ab = reinterpret_cast<float4*>(tile_base(c, F, acc, tr, tc));
@@ -241,6 +244,45 @@ __global__ void __launch_bounds__(256) k_trunc_commit(Ctx c, PktDev in, BufDev a
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(256) k_trunc_commit(Ctx c, PktDev in, BufDev acc, BufDev trunc,
+                                                      const unsigned* __restrict__ tile_max, float thr, int relu,
+                                                      PktDev out) {
+    pdl_enter();
+    __shared__ int s_list[kMaxList];
+    __shared__ int s_warp[8];
+    const FrameDev& F = *c.f;
+    const int nl = build_tile_list(c, F, in, true, s_list, s_warp);
+    commit_body(c, F, in, acc, trunc, tile_max, thr, relu, out, s_list, nl);
+}
+
+// Both passes in ONE cooperative persistent launch (every CTA resident): the
+// tile list is built once, and a grid barrier separates the tile maxima from
+// their use, saving a kernel boundary and its latency chain per layer.
+__device__ __forceinline__ void grid_barrier(unsigned* ctr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        while (atomicAdd(ctr, 0u) < gridDim.x) __nanosleep(64);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_trunc_coop(Ctx c, PktDev in, BufDev acc, BufDev trunc,
+                                                    unsigned* __restrict__ tile_max, float thr, int relu, PktDev out,
+                                                    unsigned* __restrict__ gbar) {
+    pdl_enter();
+    __shared__ int s_list[kMaxList];
+    __shared__ int s_warp[8];
+    const FrameDev& F = *c.f;
+    ring_add_part(c, F, in, trunc, blockIdx.x * (long long)blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
+    const int nl = build_tile_list(c, F, in, true, s_list, s_warp);
+    tilemax_body(c, F, in, trunc, tile_max, s_list, nl);
+    grid_barrier(gbar);
+    commit_body(c, F, in, acc, trunc, tile_max, thr, relu, out, s_list, nl);
 }
 
 // Max pool, halo-free input, k == stride (network.cpp:164-166), C % 4 == 0:
@@ -321,8 +363,29 @@ int stream_grid(K kernel) {
 }  // namespace
 
 bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
-                           float thr, int relu, PktDev out) {
+                           float thr, int relu, PktDev out, unsigned* gbar) {
     if ((in.C & 3) != 0) return false;
+    static const int gc = stream_grid(k_trunc_coop);
+    static const bool coop_ok = [] {
+        const char* e = getenv("DFX_TRUNC_COOP");
+        return !(e && e[0] == '0');
+    }();
+    if (gbar && coop_ok) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(gc);
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl_enabled() ? 2 : 1;
+        if (cudaLaunchKernelEx(&cfg, k_trunc_coop, c, in, acc, trunc, tile_max, thr, relu, out, gbar) == cudaSuccess)
+            return true;
+        cudaGetLastError();  // fall back to two launches
+    }
     static const int g1 = stream_grid(k_trunc_tilemax), g2 = stream_grid(k_trunc_commit);
     launch_pdl(k_trunc_tilemax, g1, 256, 0, s, c, in, trunc, tile_max);
     launch_pdl(k_trunc_commit, g2, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out);
