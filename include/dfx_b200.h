@@ -21,6 +21,7 @@
  *   dfx_engine_read_packet   the per-layer DeltaPacket the observer sees  engine.hpp:69-70, engine.cpp:239,279
  *   dfx_engine_read_ledger   DeltaEngine::ledger()                     engine.hpp:64 (TileLedger, buffer_manager.hpp:13-88)
  *   dfx_wrap_tile            dflx::wrap_tile                            tile_grid.hpp:37-40
+ *   dfx_ledger_*             dflx::TileLedger + plan_frame + apply_plan buffer_manager.hpp:13-126
  *
  * Conventions: every call returns 0 on success and a nonzero dfx_status on
  * failure; dfx_last_error() returns a thread-local message (C++ exceptions
@@ -228,6 +229,20 @@ int dfx_engine_timer_start(dfx_engine* e);
 int dfx_engine_timer_stop(dfx_engine* e, float* ms);
 
 void dfx_wrap_tile(int64_t tx, int64_t ty, int rows, int cols, int* row, int* col);
+
+/* Host-only tile ledger: the TileLedger / plan_frame / apply_plan the engine
+ * plans every frame with (buffer_manager.hpp:13-126, buffer_manager.cpp:7-81;
+ * full reset + replan as engine.cpp:207-211). dfx_ledger_step plans and
+ * applies one placement; claims are (tx, ty, victim_tx, victim_ty) with
+ * victims[i] = 1 when the claim evicts; fresh tiles are (tx, ty). Slot
+ * readback order is row-major over (floor_mod(ty, rows), floor_mod(tx, cols)). */
+typedef struct dfx_ledger dfx_ledger;
+int dfx_ledger_create(int rows, int cols, dfx_ledger** out);
+int dfx_ledger_destroy(dfx_ledger* h);
+int dfx_ledger_step(dfx_ledger* h, int64_t otx, int64_t oty, int th, int tw, int ring, int* full_reset,
+                    int64_t* claims, int* victims, size_t claim_cap, int* nclaims, int64_t* fresh, size_t fresh_cap,
+                    int* nfresh, int* evicted);
+int dfx_ledger_slots(dfx_ledger* h, int* used, int64_t* ty, int64_t* tx, uint8_t* covered, size_t cap);
 
 #ifdef __cplusplus
 }

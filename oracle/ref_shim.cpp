@@ -364,4 +364,74 @@ int dfr_run_streams(const dfx_net_desc* net, const dfx_engine_config* cfg, int s
     }
 }
 
+// Unmodified reference TileLedger / plan_frame / apply_plan (engine semantics
+// for the full reset: engine.cpp:207-211), same signatures as dfx_ledger_*.
+struct RefLedger {
+    TileLedger l;
+};
+int dfr_ledger_create(int rows, int cols, void** out) {
+    try {
+        auto* h = new RefLedger;
+        h->l = TileLedger(rows, cols);
+        *out = h;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_with(e);
+    }
+}
+int dfr_ledger_destroy(void* h) {
+    delete static_cast<RefLedger*>(h);
+    return 0;
+}
+int dfr_ledger_step(void* hv, int64_t otx, int64_t oty, int th, int tw, int ring, int* full_reset, int64_t* claims,
+                    int* victims, size_t claim_cap, int* nclaims, int64_t* fresh, size_t fresh_cap, int* nfresh,
+                    int* evicted) {
+    try {
+        auto* h = static_cast<RefLedger*>(hv);
+        FramePlacement place;
+        place.origin = TileCoord{otx, oty};
+        place.tiles_h = th;
+        place.tiles_w = tw;
+        FramePlan plan = plan_frame(h->l, place, ring);
+        *full_reset = plan.needs_full_reset ? 1 : 0;
+        if (plan.needs_full_reset) {
+            h->l.clear();
+            plan = plan_frame(h->l, place, ring);
+        }
+        apply_plan(plan, h->l, [](const TileCoord&) {});
+        *nclaims = (int)plan.claims.size();
+        *nfresh = (int)plan.fresh_tiles.size();
+        *evicted = (int)plan.evicted_tiles.size();
+        for (size_t i = 0; i < plan.claims.size() && i < claim_cap; ++i) {
+            claims[4 * i] = plan.claims[i].coord.tx;
+            claims[4 * i + 1] = plan.claims[i].coord.ty;
+            claims[4 * i + 2] = plan.claims[i].evicts ? plan.claims[i].evicts->tx : 0;
+            claims[4 * i + 3] = plan.claims[i].evicts ? plan.claims[i].evicts->ty : 0;
+            victims[i] = plan.claims[i].evicts ? 1 : 0;
+        }
+        for (size_t i = 0; i < plan.fresh_tiles.size() && i < fresh_cap; ++i) {
+            fresh[2 * i] = plan.fresh_tiles[i].tx;
+            fresh[2 * i + 1] = plan.fresh_tiles[i].ty;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_with(e);
+    }
+}
+int dfr_ledger_slots(void* hv, int* used, int64_t* ty, int64_t* tx, uint8_t* covered, size_t cap) {
+    auto* h = static_cast<RefLedger*>(hv);
+    const size_t n = (size_t)h->l.rows() * h->l.cols();
+    if (cap < n) return DFX_ERR;
+    for (int r = 0; r < h->l.rows(); ++r)
+        for (int c = 0; c < h->l.cols(); ++c) {
+            const auto& s = h->l.slot_local(r, c);
+            const size_t i = (size_t)r * h->l.cols() + c;
+            used[i] = s.used ? 1 : 0;
+            ty[i] = s.coord.ty;
+            tx[i] = s.coord.tx;
+            covered[i] = s.covered ? 1 : 0;
+        }
+    return 0;
+}
+
 }  // extern "C"

@@ -1292,6 +1292,67 @@ int dfx_engine_read_packet(dfx_engine* e, const char* layer, float* out, size_t 
 int dfx_engine_read_ledger(dfx_engine* e, int* used, int64_t* ty, int64_t* tx, uint8_t* covered, size_t cap) {
     return guard([&] { e->e->read_ledger(used, ty, tx, covered, cap); });
 }
+// ---- host-only ledger (TileLedger + plan_frame + apply_plan, buffer_manager.cpp:7-81),
+// the same object the engine plans every frame with; exposed for parity fuzzing.
+struct dfx_ledger {
+    dfx::Ledger l;
+};
+int dfx_ledger_create(int rows, int cols, dfx_ledger** out) {
+    return guard([&] {
+        dfx::check(rows >= 1 && cols >= 1, "ledger: bad grid dims");
+        auto* h = new dfx_ledger;
+        h->l.init(rows, cols);
+        *out = h;
+    });
+}
+int dfx_ledger_destroy(dfx_ledger* h) {
+    return guard([&] { delete h; });
+}
+int dfx_ledger_step(dfx_ledger* h, int64_t otx, int64_t oty, int th, int tw, int ring, int* full_reset,
+                    int64_t* claims, int* victims, size_t claim_cap, int* nclaims, int64_t* fresh, size_t fresh_cap,
+                    int* nfresh, int* evicted) {
+    return guard([&] {
+        dfx::Placement p;
+        p.origin = {otx, oty};
+        p.th = th;
+        p.tw = tw;
+        dfx::check(th <= h->l.rows() && tw <= h->l.cols(), "plan_frame: placement larger than grid");
+        dfx::Plan plan = h->l.plan(p, ring);
+        *full_reset = plan.full_reset ? 1 : 0;
+        if (plan.full_reset) {  // engine.cpp:207-211
+            h->l.clear();
+            plan = h->l.plan(p, ring);
+        }
+        h->l.apply(plan, p);
+        *nclaims = (int)plan.claims.size();
+        *nfresh = (int)plan.fresh.size();
+        *evicted = plan.evicted;
+        for (size_t i = 0; i < plan.claims.size() && i < claim_cap; ++i) {
+            claims[4 * i] = plan.claims[i].coord.tx;
+            claims[4 * i + 1] = plan.claims[i].coord.ty;
+            claims[4 * i + 2] = plan.claims[i].evicts ? plan.claims[i].victim.tx : 0;
+            claims[4 * i + 3] = plan.claims[i].evicts ? plan.claims[i].victim.ty : 0;
+            victims[i] = plan.claims[i].evicts ? 1 : 0;
+        }
+        for (size_t i = 0; i < plan.fresh.size() && i < fresh_cap; ++i) {
+            fresh[2 * i] = plan.fresh[i].tx;
+            fresh[2 * i + 1] = plan.fresh[i].ty;
+        }
+    });
+}
+int dfx_ledger_slots(dfx_ledger* h, int* used, int64_t* ty, int64_t* tx, uint8_t* covered, size_t cap) {
+    return guard([&] {
+        const auto& s = h->l.slots();
+        dfx::check(cap >= s.size(), "ledger slots buffer too small");
+        for (size_t i = 0; i < s.size(); ++i) {
+            used[i] = s[i].used ? 1 : 0;
+            ty[i] = s[i].coord.ty;
+            tx[i] = s[i].coord.tx;
+            covered[i] = s[i].covered ? 1 : 0;
+        }
+    });
+}
+
 // Debug: clock64 stamps of the last dense conv launch (DFX_CONV_DBG & 64).
 int dfx_debug_conv_trace(long long* out, int n) {
     return guard([&] {
