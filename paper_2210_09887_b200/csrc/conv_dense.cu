@@ -628,19 +628,33 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                         if (!(y >= -hs && y < eh && x >= -hs && x < ew)) continue;
                         float* dst = a.out.d + pkt_off(a.out, y, x);
                         const int o1 = min(a.cout, (nb + 1) * a.NBD);
-                        for (int o = nb * a.NBD; o < o1; o += 4) {
-                            const float* src = a.ws + ((size_t)u * 128 + m) * a.cout_pad + o;
-                            float4 acc4 = __ldcg(reinterpret_cast<const float4*>(src));
+                        const size_t sstride = (size_t)n * 128 * a.cout_pad;
+                        // 8 float4 per split in flight per step (the partials sit in L2)
+                        for (int ob = nb * a.NBD; ob < o1; ob += 32) {
+                            const float* src = a.ws + ((size_t)u * 128 + m) * a.cout_pad + ob;
+                            float4 acc4[8];
+#pragma unroll
+                            for (int q4 = 0; q4 < 8; ++q4) acc4[q4] = __ldcg(reinterpret_cast<const float4*>(src) + q4);
                             for (int sp = 1; sp < S; ++sp) {
-                                const float4 v = __ldcg(reinterpret_cast<const float4*>(src + (size_t)sp * n * 128 * a.cout_pad));
-                                acc4.x = __fadd_rn(acc4.x, v.x), acc4.y = __fadd_rn(acc4.y, v.y);
-                                acc4.z = __fadd_rn(acc4.z, v.z), acc4.w = __fadd_rn(acc4.w, v.w);
+                                float4 v[8];
+#pragma unroll
+                                for (int q4 = 0; q4 < 8; ++q4)
+                                    v[q4] = __ldcg(reinterpret_cast<const float4*>(src + sp * sstride) + q4);
+#pragma unroll
+                                for (int q4 = 0; q4 < 8; ++q4) {
+                                    acc4[q4].x = __fadd_rn(acc4[q4].x, v[q4].x), acc4[q4].y = __fadd_rn(acc4[q4].y, v[q4].y);
+                                    acc4[q4].z = __fadd_rn(acc4[q4].z, v[q4].z), acc4[q4].w = __fadd_rn(acc4[q4].w, v[q4].w);
+                                }
                             }
-                            if ((a.out.C & 3) == 0 && o + 4 <= o1) {
-                                *reinterpret_cast<float4*>(dst + o) = acc4;
-                            } else {
-                                const float vv[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
-                                for (int e = 0; e < 4 && o + e < o1; ++e) dst[o + e] = vv[e];
+#pragma unroll
+                            for (int q4 = 0; q4 < 8; ++q4) {
+                                const int o = ob + 4 * q4;
+                                if ((a.out.C & 3) == 0 && o + 4 <= o1) {
+                                    *reinterpret_cast<float4*>(dst + o) = acc4[q4];
+                                } else {
+                                    const float vv[4] = {acc4[q4].x, acc4[q4].y, acc4[q4].z, acc4[q4].w};
+                                    for (int e = 0; e < 4 && o + e < o1; ++e) dst[o + e] = vv[e];
+                                }
                             }
                         }
                     }
