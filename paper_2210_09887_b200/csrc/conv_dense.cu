@@ -806,7 +806,7 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     const long long wbytes = (long long)cin * cout * k * k * 8;
     p.umax = 1;  // measured: one unit per item wins on the C2 layers (DFX_DENSE_UMAX=2 to compare)
     (void)wbytes;
-    if (const char* u = getenv("DFX_DENSE_UMAX")) p.umax = atoi(u) >= 2 ? 2 : 1;
+    if (const char* u = getenv("DFX_DENSE_UMAX")) p.umax = (atoi(u) >= 2 && p.cin_pad % 16 == 0) ? 2 : 1;
     p.KC = p.umax == 2 ? 16 : (p.cin_pad % 32 == 0 ? 32 : (p.cin_pad % 16 == 0 ? 16 : 8));
     p.nCB = p.cin_pad / p.KC;
     p.r = k / 2;
