@@ -704,11 +704,12 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                     // stride-1 conv: 16x8-pixel units with >= tau targets computed whole
                     // (k_conv_dense); at tiles >= 16 px the 1-px ring strips of sparser
                     // units go to the gathered kernel instead of wasting whole units
-                    const int tau = l.tile >= 16 ? 48 : 1;
+                    static const int tau_env = getenv("DFX_DENSE_TAU") ? atoi(getenv("DFX_DENSE_TAU")) : -1;
+                    const int tau = tau_env >= 1 ? tau_env : (l.tile >= 16 ? 48 : 1);
                     PROF(DFX_FAM_CONV_TARGETS, launch_conv_plan(C, s, rt.dp, a, rt.pkt, rt.halo_geom, rt.units.p,
                                                                 ucounts + idx2, flop_px + idx2, tau, rt.list.p,
                                                                 counts + idx2));
-                    if (tau > 1)
+                    if (tau > 1 && l.stride == 1)
                         PROF(DFX_FAM_CONV_MMA, launch_conv_tc(C, s, a, rt.wtc.p, l.cin, rt.cin_pad, l.cout, rt.cout_pad,
                                                               l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom, rt.list.p,
                                                               counts + idx2, rt.max_targets, num_sms_, rt.ws.p,
