@@ -795,6 +795,9 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     p.cin_pad = (cin + 7) / 8 * 8;
     p.cout_pad = (cout + 31) / 32 * 32;
     p.NBD = p.cout_pad < 128 ? p.cout_pad : 128;
+    if (const char* nb = getenv("DFX_DENSE_NBD")) {  // experiments: N = 256 MMAs for wide layers
+        if (atoi(nb) == 256 && p.cout_pad % 256 == 0) p.NBD = 256;
+    }
     if (p.cout_pad % p.NBD) p.NBD = 32;
     p.nNB = p.cout_pad / p.NBD;
     // One unit per item (measured best on the C2 layers: more SMs busy, and

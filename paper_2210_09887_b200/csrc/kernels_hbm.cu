@@ -260,13 +260,18 @@ __global__ void __launch_bounds__(256) k_trunc_commit(Ctx c, PktDev in, BufDev a
 // Both passes in ONE cooperative persistent launch (every CTA resident): the
 // tile list is built once, and a grid barrier separates the tile maxima from
 // their use, saving a kernel boundary and its latency chain per layer.
+// One arrival per CTA (release), then acquire LOADS while waiting: polling with
+// read-modify-write atomics from every CTA would serialise at the L2 slice.
 __device__ __forceinline__ void grid_barrier(unsigned* ctr) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(ctr, 1u);
-        while (atomicAdd(ctr, 0u) < gridDim.x) __nanosleep(64);
-        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+        unsigned v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (v >= gridDim.x) break;
+            __nanosleep(32);
+        }
     }
     __syncthreads();
 }
