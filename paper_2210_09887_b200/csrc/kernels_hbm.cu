@@ -128,21 +128,31 @@ __device__ int build_tile_list(const Ctx& c, const FrameDev& F, const PktDev& p,
 }
 
 // Delta packet float4 of tile element e4 (tile row-major [yy][xx][c]).
-__device__ __forceinline__ const float4* pkt_f4(const PktDev& p, int tr, int tc, int e4, int row4) {
-    const int yy = e4 / row4, rem = e4 - yy * row4;
+struct Div {
+    int d, sh;
+    __device__ __forceinline__ explicit Div(int v) : d(v), sh(-1) {
+        if (v > 0 && (v & (v - 1)) == 0) {
+            sh = 0;
+            while ((1 << sh) < v) ++sh;
+        }
+    }
+    __device__ __forceinline__ int operator()(int x) const { return sh >= 0 ? (x >> sh) : x / d; }
+};
+__device__ __forceinline__ const float4* pkt_f4(const PktDev& p, int tr, int tc, int e4, const Div& row4) {
+    const int yy = row4(e4), rem = e4 - yy * row4.d;
     return reinterpret_cast<const float4*>(p.d + pkt_off(p, tr * p.t + yy, tc * p.t)) + rem;
 }
 
 // Pass 1 of the truncation: max |trunc + delta| per masked owned tile.
 __device__ void tilemax_body(const Ctx& c, const FrameDev& F, const PktDev& in, BufDev trunc,
                              unsigned* __restrict__ tile_max, const int* s_list, int nl) {
-    const int T = in.t, E4 = T * T * in.C / 4, row4 = T * in.C / 4;
-    const int nch = (E4 + kChunkF4 - 1) / kChunkF4;
-    const int items = (nl < 0 ? F.th * F.tw : nl) * nch;
+    const int T = in.t, E4 = T * T * in.C / 4;
+    const Div row4(T * in.C / 4), nch((E4 + kChunkF4 - 1) / kChunkF4);
+    const int items = (nl < 0 ? F.th * F.tw : nl) * nch.d;
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     for (int it = gw; it < items; it += nw) {
-        const int li = it / nch, ch = it - li * nch;
+        const int li = nch(it), ch = it - li * nch.d;
         const int ti = nl < 0 ? li : s_list[li];
         const int tr = ti / F.tw, tc = ti - tr * F.tw;
         if (nl < 0 && (!in.ext[ext_idx(in, tr, tc)] || !holds_t(c, F, tr, tc))) continue;
@@ -183,8 +193,8 @@ __global__ void __launch_bounds__(256) k_trunc_tilemax(Ctx c, PktDev in, BufDev 
 __device__ void commit_body(const Ctx& c, const FrameDev& F, const PktDev& in, BufDev acc, BufDev trunc,
                             const unsigned* __restrict__ tile_max, float thr, int relu, const PktDev& out,
                             const int* s_list, int nl) {
-    const int T = in.t, E4 = T * T * in.C / 4, row4 = T * in.C / 4;
-    const int nch = (E4 + kChunkF4 - 1) / kChunkF4;
+    const int T = in.t, E4 = T * T * in.C / 4;
+    const Div row4(T * in.C / 4), nch((E4 + kChunkF4 - 1) / kChunkF4);
     // output mask = fired tiles (delta_layers.cpp:203-204), every placement tile
     for (int ti = blockIdx.x * blockDim.x + threadIdx.x; ti < F.th * F.tw; ti += gridDim.x * blockDim.x) {
         const int tr = ti / F.tw, tc = ti - tr * F.tw;
@@ -192,11 +202,11 @@ __device__ void commit_body(const Ctx& c, const FrameDev& F, const PktDev& in, B
         out.ext[ext_idx(out, tr, tc)] =
             (in.ext[ext_idx(in, tr, tc)] && holds_t(c, F, tr, tc) && tm >= thr && tm > 0.0f) ? 1 : 0;
     }
-    const int items = (nl < 0 ? F.th * F.tw : nl) * nch;
+    const int items = (nl < 0 ? F.th * F.tw : nl) * nch.d;
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     for (int it = gw; it < items; it += nw) {
-        const int li = it / nch, ch = it - li * nch;
+        const int li = nch(it), ch = it - li * nch.d;
         const int ti = nl < 0 ? li : s_list[li];
         const int tr = ti / F.tw, tc = ti - tr * F.tw;
         if (nl < 0 && (!in.ext[ext_idx(in, tr, tc)] || !holds_t(c, F, tr, tc))) continue;
@@ -235,7 +245,7 @@ __device__ void commit_body(const Ctx& c, const FrameDev& F, const PktDev& in, B
                     }
                     __stcs(ab + q, nv);
                     __stcs(tb + q, make_float4(0.f, 0.f, 0.f, 0.f));
-                    const int yy = q / row4, rem = q - yy * row4;
+                    const int yy = row4(q), rem = q - yy * row4.d;
                     reinterpret_cast<float4*>(out.d + pkt_off(out, tr * T + yy, tc * T))[rem] = o;
                 } else {
                     __stcs(tb + q, cd);
