@@ -211,12 +211,15 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if torch.cuda.device_count() >= world:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # ranks sharing a GPU (testing the multi-rank path on a 1-GPU box): NCCL forbids it
+            dist.init_process_group("gloo")
 
     W, K, S = args.warmup, args.steps, max(1, args.streams)
     from paper_2210_09887_b200.streams import partition
@@ -253,11 +256,10 @@ def run_ours(args):
             eng.sync()
     torch.cuda.synchronize()
     kernels_per_step = engs[0].kernel_count()
-    ms_t = torch.tensor([ms], device=dev)
+    from paper_2210_09887_b200.streams import max_over_ranks
     if dist:
         dist.barrier()
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    ms_max = max_over_ranks(ms, dist)
     value = world * S * K / (ms_max / 1000.0)
     eng = engs[0]
 
@@ -307,10 +309,7 @@ def run_ours(args):
     ms2 = max(ms2, (time.time() - t_wall) * 1e3)
     for p in [p for hf in hframes for p in hf] + [p for ho in houts for p in ho]:
         capi["host_free"](p)
-    ms2_t = torch.tensor([ms2], device=dev)
-    if dist:
-        dist.all_reduce(ms2_t, op=dist.ReduceOp.MAX)
-    e2e_value = world * S * K / (float(ms2_t.item()) / 1000.0)
+    e2e_value = world * S * K / (max_over_ranks(ms2, dist) / 1000.0)
 
     # ---- 3. per-family kernel times (CUDA events on the engine stream) + algorithmic work
     eng3 = dfx.DeltaEngine(spec, econf, device=local)
