@@ -324,6 +324,29 @@ __global__ void k_input_apply(Ctx c, const float* __restrict__ aligned, const ui
     float* t = tile_ptr(c, F, trunc, tr, tc);
     const int row_len = T * C;
     const int r0 = ch * rpc, r1 = min(T, r0 + rpc);
+    if ((row_len & 3) == 0) {  // 16-B vectors along the tile row (rows are contiguous in all three arrays)
+        const int rl4 = row_len / 4;
+        for (int e = threadIdx.x; e < (r1 - r0) * rl4; e += blockDim.x) {
+            const int yy = r0 + e / rl4, q = e - (e / rl4) * rl4;
+            float4* a4 = reinterpret_cast<float4*>(a + (size_t)yy * row_len) + q;
+            float4* t4 = reinterpret_cast<float4*>(t + (size_t)yy * row_len) + q;
+            const float4 al = reinterpret_cast<const float4*>(aligned + ((size_t)(tr * T + yy) * pitch + tc * T) * C)[q];
+            const float4 av = *a4, tv = *t4;
+            const float4 raw = make_float4(__fsub_rn(al.x, av.x), __fsub_rn(al.y, av.y), __fsub_rn(al.z, av.z),
+                                           __fsub_rn(al.w, av.w));
+            const float4 cd = make_float4(__fadd_rn(tv.x, raw.x), __fadd_rn(tv.y, raw.y), __fadd_rn(tv.z, raw.z),
+                                          __fadd_rn(tv.w, raw.w));
+            if (fire) {
+                *a4 = make_float4(__fadd_rn(av.x, cd.x), __fadd_rn(av.y, cd.y), __fadd_rn(av.z, cd.z),
+                                  __fadd_rn(av.w, cd.w));
+                *t4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                reinterpret_cast<float4*>(out.d + pkt_off(out, tr * T + yy, tc * T))[q] = cd;
+            } else {
+                *t4 = cd;
+            }
+        }
+        return;
+    }
     for (int e = threadIdx.x; e < (r1 - r0) * row_len; e += blockDim.x) {
         const int yy = r0 + e / row_len, rem = e % row_len;
         const size_t bi = (size_t)yy * row_len + rem;
@@ -1071,6 +1094,40 @@ __global__ void k_add(Ctx c, PktDev a, PktDev b, PktDev out) {
 }
 
 // Output = acc + trunc over the placement, CHW (delta_layers.cpp:395-400).
+// C % 8 == 0: a warp takes (8-channel group, output row); each lane one pixel:
+// 2 x 16-B reads of acc and trunc, 8 plane writes coalesced across the warp.
+__global__ void k_densify8(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ out) {
+    pdl_enter();
+    const FrameDev& F = *c.f;
+    const int t = acc.t, C = acc.C, G = C / 8;
+    const int oh = F.th * t, ow = F.tw * t;
+    const size_t plane = (size_t)oh * ow;
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int it = gw; it < G * oh; it += nw) {
+        const int g = it / oh, y = it - g * oh;
+        const int qy = y / t, yy = y - qy * t;
+        for (int x = lane; x < ow; x += 32) {
+            const int qx = x / t;
+            const size_t off = (size_t)slot_of(F, c.rows, c.cols, qy, qx) * t * t * C +
+                               ((size_t)yy * t + (x - qx * t)) * C + g * 8;
+            const float4 a0 = __ldcs(reinterpret_cast<const float4*>(acc.d + off));
+            const float4 a1 = __ldcs(reinterpret_cast<const float4*>(acc.d + off) + 1);
+            const float4 t0 = __ldcs(reinterpret_cast<const float4*>(trunc.d + off));
+            const float4 t1 = __ldcs(reinterpret_cast<const float4*>(trunc.d + off) + 1);
+            float* o = out + (size_t)(g * 8) * plane + (size_t)y * ow + x;
+            o[0] = __fadd_rn(a0.x, t0.x);
+            o[plane] = __fadd_rn(a0.y, t0.y);
+            o[2 * plane] = __fadd_rn(a0.z, t0.z);
+            o[3 * plane] = __fadd_rn(a0.w, t0.w);
+            o[4 * plane] = __fadd_rn(a1.x, t1.x);
+            o[5 * plane] = __fadd_rn(a1.y, t1.y);
+            o[6 * plane] = __fadd_rn(a1.z, t1.z);
+            o[7 * plane] = __fadd_rn(a1.w, t1.w);
+        }
+    }
+}
+
 __global__ void k_densify(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ out) {
     pdl_enter();
     const FrameDev& F = *c.f;
@@ -1230,6 +1287,10 @@ void launch_conv_exact(const Ctx& c, cudaStream_t s, PktDev in, const float* w, 
     launch_pdl(k_conv_exact, (int)g, 256, smem, s, c, in, w, cin, cout, k, st, r, out, hg, list, count, ci);
 }
 void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out) {
+    if ((acc.C & 7) == 0) {
+        launch_pdl(k_densify8, num_sms_cached() * 8, kThreads, 0, s, c, acc, trunc, out);
+        return;
+    }
     launch_pdl(k_densify, persistent_grid((long long)acc.C * c.rows * acc.t * c.cols * acc.t), kThreads, 0, s, c, acc, trunc,
                                                                                                        out);
 }
