@@ -91,9 +91,24 @@ DFX_HD size_t pkt_off(const PktDev& p, int y, int x) {
 DFX_HD int ext_idx(const PktDev& p, int i, int j) { return (i + p.RT) * p.ext_pitch + (j + p.RT); }
 
 // Slot index of placement-relative tile (qy, qx) (may be negative / beyond).
+// For 0 <= q < n (every placement tile) floor_mod(base + q, n) is one
+// conditional subtract (base is already in [0, n)): no integer division on the
+// hot path; other tiles (ring) take the general form.
 DFX_HD int slot_of(const FrameDev& f, int rows, int cols, int qy, int qx) {
-    return floor_mod32(f.base_sr + floor_mod32(qy, rows), rows) * cols +
-           floor_mod32(f.base_sc + floor_mod32(qx, cols), cols);
+    int r, s;
+    if ((unsigned)qy < (unsigned)rows) {
+        r = f.base_sr + qy;
+        r -= r >= rows ? rows : 0;
+    } else {
+        r = floor_mod32(f.base_sr + floor_mod32(qy, rows), rows);
+    }
+    if ((unsigned)qx < (unsigned)cols) {
+        s = f.base_sc + qx;
+        s -= s >= cols ? cols : 0;
+    } else {
+        s = floor_mod32(f.base_sc + floor_mod32(qx, cols), cols);
+    }
+    return r * cols + s;
 }
 
 }  // namespace dfx

@@ -1364,6 +1364,17 @@ int dfx_debug_conv_trace(long long* out, int n) {
                    "trace copy failed");
     });
 }
+// Debug: truncation phase stamps (DFX_TRUNC_TRACE=1), [64][1024][8] u64.
+int dfx_debug_trunc_trace(unsigned long long* out, long long n) {
+    return guard([&] {
+        unsigned long long* t = dfx::trunc_trace_buffer();
+        dfx::check(t != nullptr, "no trace (set DFX_TRUNC_TRACE=1)");
+        cudaDeviceSynchronize();
+        const long long cap = 64LL * 1024 * 16;
+        dfx::check(cudaMemcpy(out, t, (size_t)(n < cap ? n : cap) * 8, cudaMemcpyDeviceToHost) == cudaSuccess,
+                   "trace copy failed");
+    });
+}
 // Debug: per-layer gathered-target counts and dense-unit counts of the last frame.
 int dfx_engine_debug_counts(dfx_engine* e, int* gathered, int* units, int cap) {
     return guard([&] { e->e->debug_counts(gathered, units, cap); });

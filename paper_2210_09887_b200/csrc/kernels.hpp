@@ -108,7 +108,8 @@ void dense_conv_prepare_weights(const DenseConvPlan& p, const float* w, int cin,
 // to the gathered list (list / lcount) for launch_conv_tc (tau = 1: all dense).
 void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, int hg, int* units,
                       int* nunits, unsigned long long* flop_px, int tau, int* list, int* lcount);
-long long* dense_conv_trace_buffer();  // microbenchmark stamps (DFX_CONV_DBG & 64)
+long long* dense_conv_trace_buffer();
+unsigned long long* trunc_trace_buffer();  // DFX_TRUNC_TRACE: [64 launches][1024 CTAs][8] globaltimer stamps  // microbenchmark stamps (DFX_CONV_DBG & 64)
 void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,
                        int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms);
 

@@ -26,7 +26,11 @@ namespace dfx {
 namespace {
 
 constexpr int kSub = 8;               // float4s per lane in flight per array
-constexpr int kChunkF4 = 32 * kSub;   // float4s per warp work item (4 KB): one round, all loads issued up front
+constexpr int kChunkF4 = 32 * kSub;
+#ifndef DFX_TRUNC_PREFETCH
+#define DFX_TRUNC_PREFETCH 1
+#endif
+constexpr bool kTruncPrefetch = DFX_TRUNC_PREFETCH != 0;   // float4s per warp work item (4 KB): one round, all loads issued up front
 
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
     return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
@@ -90,21 +94,75 @@ __device__ __forceinline__ float amax4(float m, float4 v) {
 // when the placement has more tiles than the list holds (callers then test
 // every tile).
 constexpr int kMaxList = 2048;
-__device__ int build_tile_list(const Ctx& c, const FrameDev& F, const PktDev& p, bool own, int* s_list, int* s_warp) {
+// zero_out (CTA 0 only): write ext = 0 of zero_out for every tile NOT in the
+// list (their final output mask; listed tiles are written by their owner).
+// Phase trace (DFX_TRUNC_TRACE=1, development only): %globaltimer stamps per CTA.
+__device__ __forceinline__ void tstamp(unsigned long long* tr, int ph) {
+    if (tr && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        tr[blockIdx.x * 16 + ph] = t;
+    }
+}
+
+__device__ __forceinline__ void tstamp_dep(unsigned long long* tr, int ph, unsigned dep) {
+    if (tr && threadIdx.x == 0) {
+        unsigned long long t;
+        if (dep == 0x7fc00001u) tr[blockIdx.x * 16 + 15] = 0;  // in-order issue: the stamp waits for dep
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        tr[blockIdx.x * 16 + ph] = t;
+    }
+}
+constexpr int kPer = kMaxList / 256;  // tiles per thread in the list builder
+// Owned bits of this thread's kPer tiles. Per-frame parameters are uploaded by a
+// copy that precedes the frame's first kernel, so this may run BEFORE
+// griddepcontrol.wait (it overlaps the previous kernel's tail).
+__device__ __forceinline__ unsigned own_bits_pre(const Ctx& c, const FrameDev& F) {
+    const int nt = F.th * F.tw, t0 = threadIdx.x * kPer;
+    unsigned b = 0;
+    if (nt > kMaxList) return 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+        if (t0 + j < nt && c.own[t0 + j] != 0) b |= 1u << j;
+    return b;
+}
+__device__ int build_tile_list(const Ctx& c, const FrameDev& F, const PktDev& p, bool own, int* s_list, int* s_warp,
+                               const PktDev* zero_out = nullptr, const unsigned* own_pre = nullptr,
+                               unsigned long long* tr = nullptr) {
     const int nt = F.th * F.tw;
     if (nt > kMaxList) return -1;
     // each thread owns up to 8 consecutive tiles: all loads in one round
-    constexpr int kPer = kMaxList / 256;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
     const int t0 = threadIdx.x * kPer;
+    // (row, col) of the thread's tiles: one division, then an incremental walk;
+    // branch-free loads (clamped index) so all kPer issue back to back
+    int pk[kPer];
+    {
+        int r = t0 / F.tw, q = t0 - r * F.tw;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            pk[j] = r << 16 | q;
+            if (++q == F.tw) q = 0, ++r;
+        }
+    }
+    uint8_t ev[kPer], ov[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const bool ok = t0 + j < nt;
+        ev[j] = p.ext[ok ? ext_idx(p, pk[j] >> 16, pk[j] & 0xffff) : 0] & (ok ? 0xff : 0);
+        ov[j] = (!own || own_pre) ? 1 : c.own[ok ? t0 + j : 0];
+    }
     unsigned bits = 0;
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
-        const int ti = t0 + j;
-        if (ti < nt) {
-            const int tr = ti / F.tw, tc = ti - tr * F.tw;
-            if (p.ext[ext_idx(p, tr, tc)] != 0 && (!own || c.own[ti] != 0)) bits |= 1u << j;
-        }
+        const bool o = !own || (own_pre ? (*own_pre >> j & 1u) != 0 : ov[j] != 0);
+        if (ev[j] != 0 && o) bits |= 1u << j;
+    }
+    tstamp_dep(tr, 8, bits);
+    if (zero_out && blockIdx.x == 0) {
+#pragma unroll
+        for (int j = 0; j < kPer; ++j)
+            if (t0 + j < nt && !(bits >> j & 1u)) zero_out->ext[ext_idx(*zero_out, pk[j] >> 16, pk[j] & 0xffff)] = 0;
     }
     // block exclusive prefix of the per-thread counts
     int v = __popc(bits), incl = v;
@@ -113,7 +171,9 @@ __device__ int build_tile_list(const Ctx& c, const FrameDev& F, const PktDev& p,
         if (lane >= o) incl += y;
     }
     if (lane == 31) s_warp[w] = incl;
+    tstamp_dep(tr, 9, incl);
     __syncthreads();
+    tstamp(tr, 10);
     int off = 0, tot = 0;
     for (int j = 0; j < nwb; ++j) {
         off += j < w ? s_warp[j] : 0;
@@ -122,19 +182,27 @@ __device__ int build_tile_list(const Ctx& c, const FrameDev& F, const PktDev& p,
     off += incl - v;
 #pragma unroll
     for (int j = 0; j < kPer; ++j)
-        if (bits >> j & 1u) s_list[off++] = t0 + j;
+        if (bits >> j & 1u) s_list[off++] = pk[j];  // packed (row << 16 | col)
     __syncthreads();
     return tot;
+}
+
+// Tile li of a list built by build_tile_list (or every placement tile when nl < 0).
+__device__ __forceinline__ void list_tile(const FrameDev& F, const int* s_list, int nl, int li, int& ti, int& tr,
+                                          int& tc) {
+    if (nl >= 0) {
+        const int v = s_list[li];
+        tr = v >> 16, tc = v & 0xffff, ti = tr * F.tw + tc;
+    } else {
+        ti = li, tr = ti / F.tw, tc = ti - tr * F.tw;
+    }
 }
 
 // Delta packet float4 of tile element e4 (tile row-major [yy][xx][c]).
 struct Div {
     int d, sh;
     __device__ __forceinline__ explicit Div(int v) : d(v), sh(-1) {
-        if (v > 0 && (v & (v - 1)) == 0) {
-            sh = 0;
-            while ((1 << sh) < v) ++sh;
-        }
+        if (v > 0 && (v & (v - 1)) == 0) sh = __ffs(v) - 1;
     }
     __device__ __forceinline__ int operator()(int x) const { return sh >= 0 ? (x >> sh) : x / d; }
 };
@@ -144,8 +212,13 @@ __device__ __forceinline__ const float4* pkt_f4(const PktDev& p, int tr, int tc,
 }
 
 // Pass 1 of the truncation: max |trunc + delta| per masked owned tile.
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 __device__ void tilemax_body(const Ctx& c, const FrameDev& F, const PktDev& in, BufDev trunc,
-                             unsigned* __restrict__ tile_max, const int* s_list, int nl) {
+                             unsigned* __restrict__ tile_max, const int* s_list, int nl,
+                             const float* acc_prefetch = nullptr, int acc_C = 0, unsigned long long* trc = nullptr) {
+    bool first = true;
     const int T = in.t, E4 = T * T * in.C / 4;
     const Div row4(T * in.C / 4), nch((E4 + kChunkF4 - 1) / kChunkF4);
     const int items = (nl < 0 ? F.th * F.tw : nl) * nch.d;
@@ -153,11 +226,17 @@ __device__ void tilemax_body(const Ctx& c, const FrameDev& F, const PktDev& in, 
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     for (int it = gw; it < items; it += nw) {
         const int li = nch(it), ch = it - li * nch.d;
-        const int ti = nl < 0 ? li : s_list[li];
-        const int tr = ti / F.tw, tc = ti - tr * F.tw;
+        int ti, tr, tc;
+        list_tile(F, s_list, nl, li, ti, tr, tc);
         if (nl < 0 && (!in.ext[ext_idx(in, tr, tc)] || !holds_t(c, F, tr, tc))) continue;
         const float4* tb = reinterpret_cast<const float4*>(tile_base(c, F, trunc, tr, tc));
         const int q0 = ch * kChunkF4, q1 = min(E4, q0 + kChunkF4);
+        if (first) tstamp_dep(trc, 11, (unsigned)(size_t)tb);
+        if (acc_prefetch) {  // the commit pass reads acc of fired tiles: start it towards L2 now
+            const float4* ab = reinterpret_cast<const float4*>(acc_prefetch + (size_t)slot_of(F, c.rows, c.cols, tr, tc) *
+                                                                               T * T * acc_C);
+            for (int q = q0 + lane * 8; q < q1; q += 256) prefetch_l2(ab + q);
+        }
         float m = 0.0f;
         for (int qs = q0; qs < q1; qs += 32 * kSub) {
             float4 tv[kSub], dv[kSub];
@@ -169,10 +248,13 @@ __device__ void tilemax_body(const Ctx& c, const FrameDev& F, const PktDev& in, 
                     dv[j] = __ldcg(pkt_f4(in, tr, tc, q, row4));
                 }
             }
+            if (first) tstamp_dep(trc, 12, __float_as_uint(tv[0].x) ^ __float_as_uint(dv[0].x));
 #pragma unroll
             for (int j = 0; j < kSub; ++j)
                 if (qs + j * 32 + lane < q1) m = amax4(m, add4(tv[j], dv[j]));
         }
+        if (first) tstamp_dep(trc, 13, __float_as_uint(m));
+        first = false;
         for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
         if (lane == 0 && m > 0.0f) atomicMax(tile_max + ti, __float_as_uint(m));
     }
@@ -192,10 +274,11 @@ __global__ void __launch_bounds__(256) k_trunc_tilemax(Ctx c, PktDev in, BufDev 
 // Pass 2: output mask of every placement tile, then fire / fold of the masked ones.
 __device__ void commit_body(const Ctx& c, const FrameDev& F, const PktDev& in, BufDev acc, BufDev trunc,
                             const unsigned* __restrict__ tile_max, float thr, int relu, const PktDev& out,
-                            const int* s_list, int nl) {
+                            const int* s_list, int nl, bool ext_by_items = false) {
     const int T = in.t, E4 = T * T * in.C / 4;
     const Div row4(T * in.C / 4), nch((E4 + kChunkF4 - 1) / kChunkF4);
     // output mask = fired tiles (delta_layers.cpp:203-204), every placement tile
+    if (!ext_by_items || nl < 0)
     for (int ti = blockIdx.x * blockDim.x + threadIdx.x; ti < F.th * F.tw; ti += gridDim.x * blockDim.x) {
         const int tr = ti / F.tw, tc = ti - tr * F.tw;
         const float tm = __uint_as_float(__ldcg(tile_max + ti));
@@ -207,11 +290,12 @@ __device__ void commit_body(const Ctx& c, const FrameDev& F, const PktDev& in, B
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     for (int it = gw; it < items; it += nw) {
         const int li = nch(it), ch = it - li * nch.d;
-        const int ti = nl < 0 ? li : s_list[li];
-        const int tr = ti / F.tw, tc = ti - tr * F.tw;
+        int ti, tr, tc;
+        list_tile(F, s_list, nl, li, ti, tr, tc);
         if (nl < 0 && (!in.ext[ext_idx(in, tr, tc)] || !holds_t(c, F, tr, tc))) continue;
         const float tm = __uint_as_float(__ldcg(tile_max + ti));
         const bool fire = tm >= thr && tm > 0.0f;
+        if (ext_by_items && nl >= 0 && ch == 0 && lane == 0) out.ext[ext_idx(out, tr, tc)] = fire ? 1 : 0;
         float4* tb = reinterpret_cast<float4*>(tile_base(c, F, trunc, tr, tc));
         float4* ab = reinterpret_cast<float4*>(tile_base(c, F, acc, tr, tc));
         const int q0 = ch * kChunkF4, q1 = min(E4, q0 + kChunkF4);
@@ -226,7 +310,8 @@ __device__ void commit_body(const Ctx& c, const FrameDev& F, const PktDev& in, B
                 if (q < q1) {
                     tv[j] = __ldcg(tb + q);
                     dv[j] = __ldcg(pkt_f4(in, tr, tc, q, row4));
-                    if (fire) pv[j] = __ldcs(ab + q);
+                    if (kTruncPrefetch) pv[j] = __ldcg(ab + q);  // L2 hit: prefetched in pass 1, no wait on tile_max
+                    else if (fire) pv[j] = __ldcs(ab + q);
                 }
             }
 #pragma unroll
@@ -288,16 +373,43 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr) {
 
 __global__ void __launch_bounds__(256) k_trunc_coop(Ctx c, PktDev in, BufDev acc, BufDev trunc,
                                                     unsigned* __restrict__ tile_max, float thr, int relu, PktDev out,
-                                                    unsigned* __restrict__ gbar) {
+                                                    unsigned* __restrict__ gbar, unsigned long long* tr, int dry) {
+    tstamp(tr, 0);
+    // touch every kernel parameter up front: their constant-bank lines miss once, together
+    asm volatile("" ::"l"(in.d), "l"(in.ext), "r"(in.C), "r"(in.t), "r"(in.halo), "r"(in.RT), "r"(in.pitch_w),
+                 "r"(in.ext_pitch), "l"(acc.d), "r"(acc.C), "r"(acc.t), "l"(trunc.d), "l"(tile_max), "f"(thr), "r"(relu));
+    asm volatile("" ::"l"(out.d), "l"(out.ext), "r"(out.C), "r"(out.halo), "r"(out.RT), "r"(out.pitch_w),
+                 "r"(out.ext_pitch), "l"(gbar), "r"(c.rows), "r"(c.cols), "l"(c.slots), "l"(c.own), "l"(c.f), "r"(dry));
+    const FrameDev F = *c.f;  // per-frame data: safe before the dependency wait (see own_bits_pre)
+    const unsigned own_pre = own_bits_pre(c, F);
+    tstamp_dep(tr, 7, own_pre);
     pdl_enter();
+    tstamp(tr, 1);
     __shared__ int s_list[kMaxList];
     __shared__ int s_warp[8];
-    const FrameDev& F = *c.f;
+    const int nl = build_tile_list(c, F, in, true, s_list, s_warp, dry ? nullptr : &out, &own_pre, dry ? nullptr : tr);
+    if (dry) return;
+    tstamp(tr, 2);
+    tilemax_body(c, F, in, trunc, tile_max, s_list, nl, kTruncPrefetch ? acc.d : nullptr, acc.C, tr);
+    tstamp(tr, 3);
+    // split grid barrier: arrive, do the halo stash (ring slots only, independent of both passes), wait
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gbar) : "memory");
     ring_add_part(c, F, in, trunc, blockIdx.x * (long long)blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
-    const int nl = build_tile_list(c, F, in, true, s_list, s_warp);
-    tilemax_body(c, F, in, trunc, tile_max, s_list, nl);
-    grid_barrier(gbar);
-    commit_body(c, F, in, acc, trunc, tile_max, thr, relu, out, s_list, nl);
+    tstamp(tr, 4);
+    if (threadIdx.x == 0) {
+        unsigned v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gbar) : "memory");
+            if (v >= gridDim.x) break;
+            __nanosleep(32);
+        }
+    }
+    __syncthreads();
+    tstamp(tr, 5);
+    commit_body(c, F, in, acc, trunc, tile_max, thr, relu, out, s_list, nl, true);
+    __syncthreads();
+    tstamp(tr, 6);
 }
 
 // Max pool, halo-free input, k == stride (network.cpp:164-166), C % 4 == 0:
@@ -323,8 +435,8 @@ __global__ void __launch_bounds__(256) k_maxpool_vec(Ctx c, PktDev in, BufDev ac
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     for (int it = gw; it < items; it += nw) {
         const int li = it / nch, ch = it - li * nch;
-        const int tix = nl < 0 ? li : s_list[li];
-        const int tr = tix / F.tw, tc = tix - tr * F.tw;
+        int tix, tr, tc;
+        list_tile(F, s_list, nl, li, tix, tr, tc);
         if (nl < 0 && !in.ext[ext_idx(in, tr, tc)]) continue;
         const bool owned = holds_t(c, F, tr, tc);
         float4* ab = owned ? reinterpret_cast<float4*>(tile_base(c, F, acc, tr, tc)) : nullptr;
@@ -377,6 +489,9 @@ int stream_grid(K kernel) {
 
 }  // namespace
 
+static unsigned long long* g_trunc_trace = nullptr;
+unsigned long long* trunc_trace_buffer() { return g_trunc_trace; }
+
 bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
                            float thr, int relu, PktDev out, unsigned* gbar) {
     if ((in.C & 3) != 0) return false;
@@ -385,6 +500,17 @@ bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, 
         const char* e = getenv("DFX_TRUNC_COOP");
         return !(e && e[0] == '0');
     }();
+    static unsigned long long* trace = [] {
+        unsigned long long* p = nullptr;
+        if (getenv("DFX_TRUNC_TRACE")) cudaMalloc(&p, sizeof(unsigned long long) * 64 * 1024 * 16);
+        return p;
+    }();
+    static int seq = 0;
+    unsigned long long* tr = trace ? trace + (size_t)(seq++ % 64) * 1024 * 16 : nullptr;
+    g_trunc_trace = trace;
+    static const bool warm = getenv("DFX_TRUNC_WARM") != nullptr;  // experiment
+    if (warm) launch_pdl(k_trunc_coop, gc, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out, gbar,
+                         (unsigned long long*)nullptr, 1);
     if (gbar && coop_ok) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(gc);
@@ -397,7 +523,7 @@ bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, 
         attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = pdl_enabled() ? 2 : 1;
-        if (cudaLaunchKernelEx(&cfg, k_trunc_coop, c, in, acc, trunc, tile_max, thr, relu, out, gbar) == cudaSuccess)
+        if (cudaLaunchKernelEx(&cfg, k_trunc_coop, c, in, acc, trunc, tile_max, thr, relu, out, gbar, tr, 0) == cudaSuccess)
             return true;
         cudaGetLastError();  // fall back to two launches
     }
