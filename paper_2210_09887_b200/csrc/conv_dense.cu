@@ -160,7 +160,8 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
                                                             int nbw, int* __restrict__ units,
                                                             int* __restrict__ nunits,
                                                             unsigned long long* __restrict__ flop_px, int tau,
-                                                            int* __restrict__ list, int* __restrict__ lcount) {
+                                                            int* __restrict__ list, int* __restrict__ lcount,
+                                                            int tile_units) {
     pdl_enter();
     __shared__ uint32_t s_bits[4096 / 32];
     __shared__ int s_ucnt[32];
@@ -212,8 +213,9 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
         for (int w = 0; w < kPlanThreads / 32; ++w) tot += s_geo[w];
         if (tot) atomicAdd(flop_px, (unsigned long long)tot);  // one global atomic per block
     }
-    // units with >= tau targets are computed whole by k_conv_dense
-    if (threadIdx.x < nun && s_ucnt[threadIdx.x] >= tau) {
+    // units with >= tau targets are computed whole by k_conv_dense (tile-unit
+    // mode: every active stored tile is listed instead, see below)
+    if (!tile_units && threadIdx.x < nun && s_ucnt[threadIdx.x] >= tau) {
         const int uy = Y0 / kUY + threadIdx.x / upr, ux = X0 / kUX + threadIdx.x % upr;
         units[atomicAdd(nunits, 1)] = ((uy + 1) << 16) | (ux + 1);
     }
@@ -237,8 +239,10 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
     }
     if (threadIdx.x < ntl) {
         const int ti = floor_div32(Y0, t) + threadIdx.x / tpr, tj = floor_div32(X0, t) + threadIdx.x % tpr;
-        if (ti >= -out.RT && ti < F.th + out.RT && tj >= -out.RT && tj < F.tw + out.RT)
+        if (ti >= -out.RT && ti < F.th + out.RT && tj >= -out.RT && tj < F.tw + out.RT) {
             out.ext[ext_idx(out, ti, tj)] = s_tstore[threadIdx.x] ? 1 : 0;
+            if (tile_units && s_tstore[threadIdx.x]) units[atomicAdd(nunits, 1)] = ((ti + 8) << 16) | (tj + 8);
+        }
     }
     // zero fill: non-target stored pixels of active tiles outside dense units
     const bool sparse_unit = __syncthreads_or(threadIdx.x < nun && s_ucnt[threadIdx.x] < tau);
@@ -277,6 +281,8 @@ struct DenseArgs {
     uint32_t w_stage;      // bytes of one weight stage (hi + lo)
     uint32_t acc_cols, nbuf, a_col0;  // TMEM plan
     int umax;              // units per item the TMEM / smem plan allows (1 or 2)
+    int tpu, tsh;          // tile-unit mode (tpu tiles of 2^tsh px per unit), tpu = 0: 16x8-px units
+    int ppx;               // pixels of one unit's patch
     long long* trace;      // microbenchmark (dbg & 64): per-K-block clock64 stamps of CTA 0
     int dbg;               // microbenchmark knobs (tools/bench_conv.cu): 1 no MMA, 2 no patch, 4 no weights
 };
@@ -287,6 +293,27 @@ struct DenseArgs {
 // spreads small layers over more SMs) and S K-splits. Cost model in K-block
 // time units: waves x K-blocks per item x (MMA time + ~300 cycles of per-K-block
 // handshake, relative), + a penalty per split for the partials' traffic.
+// Unit count of the frame: 16x8-px units are listed one by one; in tile-unit
+// mode the list holds active tiles and a unit is tpu consecutive entries.
+__device__ __forceinline__ int dense_units(const DenseArgs& a, int listed) {
+    return a.tpu ? (listed + a.tpu - 1) / a.tpu : listed;
+}
+// Output pixel of row m of unit u (false: padding row of a partial tile unit).
+__device__ __forceinline__ bool unit_pixel(const DenseArgs& a, int listed, int u, int m, int& y, int& x) {
+    if (a.tpu == 0) {
+        const int uv = __ldg(a.units + u);
+        y = ((uv >> 16) - 1) * kUY + (m >> 3), x = ((uv & 0xffff) - 1) * kUX + (m & 7);
+        return true;
+    }
+    const int s = m >> (2 * a.tsh), l = m & ((1 << (2 * a.tsh)) - 1);
+    const int li = u * a.tpu + s;
+    if (li >= listed) return false;
+    const int tv = __ldg(a.units + li);
+    y = (((tv >> 16) - 8) << a.tsh) + (l >> a.tsh);
+    x = (((tv & 0xffff) - 8) << a.tsh) + (l & ((1 << a.tsh) - 1));
+    return true;
+}
+
 struct DenseSched {
     int U, S, items;
 };
@@ -371,7 +398,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     __shared__ int s_poff[2 * 22 * 14];  // per-pixel patch source offsets (k <= 7, two units)
 
     const FrameDev& F = *c.f;
-    const int n = *a.nunits;
+    const int listed = *a.nunits;
+    const int n = dense_units(a, listed);
     const int K2 = a.k * a.k;
     const int nKB = a.nCB * K2;
     const DenseSched sch = dense_sched(n, a.nNB, nKB, a.smax, a.sms, a.umax);
@@ -379,7 +407,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     if ((int)blockIdx.x >= items) return;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int PW = kUX + 2 * a.r;
+    const int PW = a.tpu ? (1 << a.tsh) + 2 * a.r : kUX + 2 * a.r;  // patch row pitch (pixels)
     const int NST = a.nst;
     // TMEM: accumulators [nbuf][2 units][NBD] then NST A stages of [2 units][hi KC | lo KC]
     const uint32_t acc_buf = a.umax * a.NBD;
@@ -429,7 +457,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
         // latency-bound); each writes both units' A rows of its K-block.
         const int wg = warp >> 2, wq = warp & 3;
         const int m = tid & 127;  // row = unit pixel (m >> 3, m & 7)
-        const uint32_t row_off = (uint32_t)((m >> 3) * PW + (m & 7)) * a.pstr;
+        const uint32_t row_off =
+            a.tpu ? (uint32_t)((m >> (2 * a.tsh)) * PW * PW + ((m >> a.tsh) & ((1 << a.tsh) - 1)) * PW +
+                               (m & ((1 << a.tsh) - 1))) * a.pstr
+                  : (uint32_t)((m >> 3) * PW + (m & 7)) * a.pstr;
         uint32_t g = 0, pseq = 0, pst = 0, pph = 0;
         for (int it = blockIdx.x; it < items; it += gridDim.x) {
             int pr, nb, kb0, kb1;
@@ -483,30 +514,44 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
         // ------------------------------------------------ patch loaders (cp.async, zero fill, TF32 split)
         const int lt = tid - 128 * kProdWG;
         const int c4n = KC / 4;
-        const int E1 = PW * (kUY + 2 * a.r) * c4n;
+        const int P = a.ppx;  // patch pixels per unit
+        const int E1 = P * c4n;
         const bool vec = (a.in.C & 3) == 0;
         uint32_t pseq = 0;
         for (int it = blockIdx.x; it < items; it += gridDim.x) {
             int pr, nb, kb0, kb1;
             item_info(it, pr, nb, kb0, kb1);
             const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
-            int y0[2], x0[2];
+            int y0[2] = {0, 0}, x0[2] = {0, 0};
+            if (!a.tpu) {
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int uv = __ldg(a.units + UPI * pr + (j < nu ? j : 0));
-                y0[j] = ((uv >> 16) - 1) * kUY - a.r;
-                x0[j] = ((uv & 0xffff) - 1) * kUX - a.r;
+                for (int j = 0; j < 2; ++j) {
+                    const int uv = __ldg(a.units + UPI * pr + (j < nu ? j : 0));
+                    y0[j] = ((uv >> 16) - 1) * kUY - a.r;
+                    x0[j] = ((uv & 0xffff) - 1) * kUX - a.r;
+                }
             }
             const int E = E1 * nu;
             // per-pixel source offset (-1: zero) of the item's patches, once per item:
             // keeps the dependent ext-map lookups out of the per-chunk copy loop
-            const int P = PW * (kUY + 2 * a.r);
             asm volatile("bar.sync 2, 128;" ::: "memory");  // previous item's copy loop is done with s_poff
             for (int q = lt; q < P * nu; q += 128) {
                 const int j = q >= P ? 1 : 0, p = q - j * P;
-                const int py = p / PW, px = p - py * PW;
-                const int y = (j ? y0[1] : y0[0]) + py, x = (j ? x0[1] : x0[0]) + px;
-                s_poff[q] = pkt_ok(a.in, F.th, F.tw, y, x) ? (int)pkt_off(a.in, y, x) : -1;
+                int y, x;
+                bool ok = true;
+                if (a.tpu) {  // tile s of the unit, (T + 2r)^2-pixel patch per tile
+                    const int s = p / (PW * PW), l = p - s * PW * PW;
+                    const int py = l / PW, px = l - py * PW;
+                    const int li = pr * a.tpu + s;
+                    ok = li < listed;
+                    const int tv = ok ? __ldg(a.units + li) : 0;
+                    y = (((tv >> 16) - 8) << a.tsh) - a.r + py;
+                    x = (((tv & 0xffff) - 8) << a.tsh) - a.r + px;
+                } else {
+                    const int py = p / PW, px = p - py * PW;
+                    y = (j ? y0[1] : y0[0]) + py, x = (j ? x0[1] : x0[0]) + px;
+                }
+                s_poff[q] = ok && pkt_ok(a.in, F.th, F.tw, y, x) ? (int)pkt_off(a.in, y, x) : -1;
             }
             asm volatile("bar.sync 2, 128;" ::: "memory");
             for (int cb = kb0 / K2; cb <= (kb1 - 1) / K2; ++cb, ++pseq) {
@@ -576,9 +621,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
             tc_fence_after();
             for (int j = 0; j < nu; ++j) {
                 const int u = UPI * pr + j;
-                const int uv = __ldg(a.units + u);
-                const int y = ((uv >> 16) - 1) * kUY + (m >> 3), x = ((uv & 0xffff) - 1) * kUX + (m & 7);
-                const bool valid = y >= -hs && y < eh && x >= -hs && x < ew;  // stored grown extent
+                int y, x;
+                const bool row = unit_pixel(a, listed, u, m, y, x);
+                const bool valid = row && y >= -hs && y < eh && x >= -hs && x < ew;  // stored grown extent
                 float* dst_row = nullptr;
                 int lim = a.cout;
                 if (S > 1) {
@@ -623,8 +668,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                     __threadfence();
                     for (int j = 0; j < nu; ++j) {
                         const int u = UPI * pr + j;
-                        const int uv = __ldg(a.units + u);
-                        const int y = ((uv >> 16) - 1) * kUY + (m >> 3), x = ((uv & 0xffff) - 1) * kUX + (m & 7);
+                        int y, x;
+                        if (!unit_pixel(a, listed, u, m, y, x)) continue;
                         if (!(y >= -hs && y < eh && x >= -hs && x < ew)) continue;
                         float* dst = a.out.d + pkt_off(a.out, y, x);
                         const int o1 = min(a.cout, (nb + 1) * a.NBD);
@@ -760,7 +805,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
 __global__ void k_conv_dense_reduce(Ctx c, DenseArgs a) {
     pdl_enter();
     const FrameDev& F = *c.f;
-    const int n = *a.nunits;
+    const int listed = *a.nunits;
+    const int n = dense_units(a, listed);
     const int S = dense_sched(n, a.nNB, a.nCB * a.k * a.k, a.smax, a.sms, a.umax).S;
     if (S <= 1) return;
     const int hs = a.out.halo;
@@ -771,8 +817,8 @@ __global__ void k_conv_dense_reduce(Ctx c, DenseArgs a) {
         const long long row = e / a.cout;
         const int o = (int)(e - row * a.cout);
         const int u = (int)(row >> 7), m = (int)(row & 127);
-        const int uv = __ldg(a.units + u);
-        const int y = ((uv >> 16) - 1) * kUY + (m >> 3), x = ((uv & 0xffff) - 1) * kUX + (m & 7);
+        int y, x;
+        if (!unit_pixel(a, listed, u, m, y, x)) continue;
         if (y < -hs || y >= eh || x < -hs || x >= ew) continue;
         float sum = a.ws[(size_t)row * a.cout_pad + o];
         for (int sp = 1; sp < S; ++sp) sum = __fadd_rn(sum, a.ws[((size_t)sp * n * 128 + row) * a.cout_pad + o]);
@@ -816,19 +862,41 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
         const int v = atoi(kc);
         if ((v == 16 || v == 32) && p.cin_pad % v == 0) p.KC = v;
     }
-    p.nCB = p.cin_pad / p.KC;
     p.r = k / 2;
     p.k = k;
-    const int PW = kUX + 2 * p.r, PH = kUY + 2 * p.r;
-    p.s_c4 = (unsigned)p.KC * 4 + 16;  // pixel stride in a patch plane (conflict-free row reads)
-    p.patch_bytes = ((unsigned)PW * PH * p.s_c4 + 127) / 128 * 128;
-    p.w_stage = (uint32_t)p.NBD * p.KC * 8;
+    // Tile units (T = t_out in {2, 4, 8}): a unit is 128 / T^2 ACTIVE output
+    // tiles gathered from anywhere in the extent, each with its own
+    // (T + 2r)^2-pixel patch, instead of a 16 x 8-pixel block that at small T
+    // mostly covers inactive tiles (measured 2.2-3.4x computed / target pixels
+    // on the C2 deep layers). DFX_TILE_UNITS=0 restores block units.
+    p.tpu = 0;
+    p.tsh = 0;
+    {
+        const char* e = getenv("DFX_TILE_UNITS");
+        const bool on = !(e && e[0] == '0');
+        if (on && (t_out == 2 || t_out == 4 || t_out == 8)) {
+            p.tpu = 128 / (t_out * t_out);
+            p.tsh = t_out == 2 ? 1 : (t_out == 4 ? 2 : 3);
+            p.umax = 1;
+        }
+    }
+    const int PW = p.tpu ? t_out + 2 * p.r : kUX + 2 * p.r, PH = p.tpu ? t_out + 2 * p.r : kUY + 2 * p.r;
+    p.patch_px = p.tpu ? p.tpu * PW * PH : PW * PH;
     const unsigned acc = (unsigned)p.umax * p.NBD;
     const size_t budget = 200 * 1024;
+    auto set_kc = [&](int kc) {
+        p.KC = kc;
+        p.nCB = p.cin_pad / p.KC;
+        p.s_c4 = (unsigned)p.KC * 4 + 16;  // pixel stride in a patch plane (conflict-free row reads)
+        p.patch_bytes = ((unsigned)p.patch_px * p.s_c4 + 127) / 128 * 128;
+        p.w_stage = (uint32_t)p.NBD * p.KC * 8;
+    };
     auto fits = [&](int nst, unsigned nbuf) {
         return 4 * (size_t)p.umax * p.patch_bytes + (size_t)nst * p.w_stage <= budget &&
                nbuf * acc + (unsigned)nst * 2 * p.umax * p.KC <= 512;
     };
+    set_kc(p.KC);
+    if (p.KC > 8 && !fits(4, 2) && !fits(4, 1)) set_kc(8);  // large tile-unit patches: 8-channel K-blocks
     // prefer double-buffered accumulators with >= 4 stages, else single with more stages
     p.nbuf = 2;
     p.nstw = 8;
@@ -842,16 +910,22 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     p.smem = 4 * (size_t)p.umax * p.patch_bytes + (size_t)p.nstw * p.w_stage;
     const int BH = t_out > kUY ? t_out : kUY, BW = t_out > kUX ? t_out : kUX;
     p.ok = fits(p.nstw, p.nbuf) && k * k <= 49 && (k & 1) && t_out <= 64 && (BH / kUY) * (BW / kUX) <= 32 &&
-           (BH / t_out) * (BW / t_out) <= 32;
+           (BH / t_out) * (BW / t_out) <= 32 && p.patch_px * p.umax <= 2 * 22 * 14;
     // units over [-16, rows*t + hg) x [-8, cols*t + hg) (hg <= 8 px of grown halo)
     p.nux_max = (cols * t_out + 8 + kUX - 1) / kUX + 1;
     p.nuy_max = (rows * t_out + 8 + kUY - 1) / kUY + 1;
     p.units_max = p.nux_max * p.nuy_max;
+    p.ws_units = p.units_max;
+    if (p.tpu) {  // the list holds tiles (ring tiles included): size it for all of them
+        const int tiles = (rows + 16) * (cols + 16);
+        p.units_max = tiles > p.units_max ? tiles : p.units_max;
+        p.ws_units = (tiles + p.tpu - 1) / p.tpu;
+    }
     p.nbh = (rows * t_out + 8 + BH - 1) / BH + 1;
     p.nbw = (cols * t_out + 8 + BW - 1) / BW + 1;
     p.t_out = t_out;
     p.smax = 8;
-    while (p.smax > 1 && (size_t)p.smax * p.units_max * 128 * p.cout_pad * 4 > ws_budget_bytes) p.smax /= 2;
+    while (p.smax > 1 && (size_t)p.smax * p.ws_units * 128 * p.cout_pad * 4 > ws_budget_bytes) p.smax /= 2;
     return p;
 }
 
@@ -890,8 +964,9 @@ void dense_conv_prepare_weights(const DenseConvPlan& p, const float* w, int cin,
 void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, int hg, int* units,
                       int* nunits, unsigned long long* flop_px, int tau, int* list, int* lcount) {
     if (hg > 8) throw std::runtime_error("conv_plan: grown halo > 8 px");
+    if (p.tpu && out.RT >= 8) throw std::runtime_error("conv_plan: tile ring too wide for tile units");
     launch_pdl(k_conv_plan, p.nbh * p.nbw, kPlanThreads, 0, s, c, in, out, p.k, p.r, hg, p.nbw, units, nunits, flop_px,
-               tau, list, lcount);
+               tau, list, lcount, p.tpu ? 1 : 0);
 }
 
 template <int KC>
@@ -911,7 +986,7 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
     if (!p.ok) throw std::runtime_error("conv_dense: unsupported layer shape");
     DenseArgs a{in, out, w, units, nunits, p.smax > 1 ? ws : nullptr, cnt, cin, cout, p.cout_pad, p.k, p.r,
                 p.KC, p.nCB, p.NBD, p.nNB, p.nstw, p.smax > 1 ? p.smax : 1, num_sms, p.s_c4, p.patch_bytes,
-                p.w_stage, p.acc_cols, p.nbuf, p.nbuf * p.acc_cols, p.umax, nullptr, 0};
+                p.w_stage, p.acc_cols, p.nbuf, p.nbuf * p.acc_cols, p.umax, p.tpu, p.tsh, p.patch_px, nullptr, 0};
     if (getenv("DFX_CONV_DBG") && !g_trace) cudaMalloc(&g_trace, 1024 * 8);
     a.trace = g_trace;
     if (const char* d = getenv("DFX_CONV_DBG")) a.dbg = atoi(d);
@@ -921,7 +996,7 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
         const int v = atoi(d);
         if (v >= 2 && v < pp.nstw) a.nst = v;
     }
-    const long long max_items = (long long)p.units_max * p.nNB * a.smax;
+    const long long max_items = (long long)p.ws_units * p.nNB * a.smax;
     const int grid = (int)(max_items < num_sms ? (max_items < 1 ? 1 : max_items) : num_sms);
     if (p.KC == 32) launch_kc<32>(grid, p.smem, s, c, a);
     else if (p.KC == 16) launch_kc<16>(grid, p.smem, s, c, a);

@@ -406,8 +406,8 @@ void Engine::allocate(int th, int tw) {
                         rt.wdense.alloc(wd.size());
                         CUDA_CHECK(cudaMemcpy(rt.wdense.p, wd.data(), wd.size() * 4, cudaMemcpyHostToDevice));
                         rt.units.alloc(rt.dp.units_max);
-                        if (rt.dp.smax > 1) rt.wsd.alloc((size_t)rt.dp.smax * rt.dp.units_max * 128 * rt.dp.cout_pad);
-                        rt.dcnt.alloc((size_t)rt.dp.units_max * rt.dp.nNB);
+                        if (rt.dp.smax > 1) rt.wsd.alloc((size_t)rt.dp.smax * rt.dp.ws_units * 128 * rt.dp.cout_pad);
+                        rt.dcnt.alloc((size_t)rt.dp.ws_units * rt.dp.nNB);
                         CUDA_CHECK(cudaMemset(rt.dcnt.p, 0, rt.dcnt.n * sizeof(int)));
                     }
                 }
