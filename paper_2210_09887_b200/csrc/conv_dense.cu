@@ -283,6 +283,7 @@ struct DenseArgs {
     int umax;              // units per item the TMEM / smem plan allows (1 or 2)
     int tpu, tsh;          // tile-unit mode (tpu tiles of 2^tsh px per unit), tpu = 0: 16x8-px units
     int ppx;               // pixels of one unit's patch
+    int npb;               // patch ring depth (raw fp32 patches; the producers split hi / lo)
     long long* trace;      // microbenchmark (dbg & 64): per-K-block clock64 stamps of CTA 0
     int dbg;               // microbenchmark knobs (tools/bench_conv.cu): 1 no MMA, 2 no patch, 4 no weights
 };
@@ -339,6 +340,13 @@ __host__ __device__ __forceinline__ DenseSched dense_sched(int n, int nNB, int n
 // (unit, channel chunk), double buffered), 4 epilogue warps, the MMA issuer and
 // the weight producer.
 constexpr int kProdWG = 3;
+constexpr int kMaxPB = 4;  // patch ring depth limit
+// dynamic shared-memory plan of k_conv_dense (<= 224 KB = 227 KB per CTA minus
+// ~3 KB static); measured: 200 KB beats 224 KB on C2 (more weight stages do not pay)
+#ifndef DFX_DENSE_SMEM_KB
+#define DFX_DENSE_SMEM_KB 200
+#endif
+constexpr size_t kDenseSmemBudget = (size_t)DFX_DENSE_SMEM_KB * 1024;
 constexpr int kDenseThreads = (4 * kProdWG + 10) * 32;
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
@@ -392,7 +400,7 @@ template <int KC>
 __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArgs a) {
     pdl_enter();
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bar_full[8], bar_empty[8], bar_pf[2], bar_pe[2], bar_af[2], bar_ae[2];
+    __shared__ __align__(8) uint64_t bar_full[8], bar_empty[8], bar_pf[kMaxPB], bar_pe[kMaxPB], bar_af[2], bar_ae[2];
     __shared__ uint32_t tmem_base_sh;
     __shared__ int s_last;
     __shared__ int s_poff[2 * 22 * 14];  // per-pixel patch source offsets (k <= 7, two units)
@@ -422,9 +430,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
             mbar_init(smem_u32(&bar_full[i]), 5);  // 4 A-producer warps + the weight bytes
             mbar_init(smem_u32(&bar_empty[i]), 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < a.npb; ++i) {
             mbar_init(smem_u32(&bar_pf[i]), 4);
             mbar_init(smem_u32(&bar_pe[i]), 4 * kProdWG);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(smem_u32(&bar_af[i]), 1);
             mbar_init(smem_u32(&bar_ae[i]), 4);
         }
@@ -437,8 +447,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     const uint32_t sbase = smem_u32(smem);
     if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) a.trace[500] = clock64();
     // smem: patches [2 buffers][2 units][hi, lo] planes, then the weight stages
-    const uint32_t unit_bytes = 2 * a.patch_bytes, buf_bytes = a.umax * unit_bytes;
-    const uint32_t w_base = sbase + 2 * buf_bytes;
+    const uint32_t unit_bytes = a.patch_bytes, buf_bytes = a.umax * unit_bytes;
+    const uint32_t w_base = sbase + a.npb * buf_bytes;
 
     // item -> (unit pair, N-block, K split) and its K-block range (channel chunk outer, tap inner)
     auto item_info = [&](int it, int& pr, int& nb, int& kb0, int& kb1) {
@@ -467,8 +477,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
             item_info(it, pr, nb, kb0, kb1);
             const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
             for (int cb = kb0 / K2; cb <= (kb1 - 1) / K2; ++cb, ++pseq) {
-                const int pb = pseq & 1;
-                mbar_wait(smem_u32(&bar_pf[pb]), (pseq >> 1) & 1);
+                const uint32_t pb = pseq % a.npb;
+                mbar_wait(smem_u32(&bar_pf[pb]), (pseq / a.npb) & 1);
                 const uint32_t patch = sbase + pb * buf_bytes + row_off;
                 const int t0 = max(kb0 - cb * K2, 0), t1 = min(kb1 - cb * K2, K2);
                 for (int tap = t0; tap < t1; ++tap, ++g) {
@@ -483,18 +493,24 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                     const long long t_b = clock64();
                     tc_fence_after();
                     for (int j = 0; j < nu; ++j) {
+                        // raw fp32 row -> hi = x with 13 low mantissa bits cleared (exact
+                        // TF32), lo = x - hi (exact; the tensor core reads its top 19 bits)
+                        uint32_t hv[KC], lv[KC];
+                        const uint32_t src = src0 + j * unit_bytes;
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {  // hi plane, then lo plane
-                            uint32_t v[KC];
-                            const uint32_t src = src0 + j * unit_bytes + h * a.patch_bytes;
+                        for (int q4 = 0; q4 < KC / 4; ++q4)
+                            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                                         : "=r"(hv[4 * q4]), "=r"(hv[4 * q4 + 1]), "=r"(hv[4 * q4 + 2]),
+                                           "=r"(hv[4 * q4 + 3])
+                                         : "r"(src + 16 * q4));
 #pragma unroll
-                            for (int q4 = 0; q4 < KC / 4; ++q4)
-                                asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                                             : "=r"(v[4 * q4]), "=r"(v[4 * q4 + 1]), "=r"(v[4 * q4 + 2]),
-                                               "=r"(v[4 * q4 + 3])
-                                             : "r"(src + 16 * q4));
-                            store_cols<KC>(taddr + j * 2 * KC + h * KC, v);
+                        for (int e = 0; e < KC; ++e) {
+                            const float x = __uint_as_float(hv[e]);
+                            hv[e] &= 0xffffe000u;
+                            lv[e] = __float_as_uint(__fsub_rn(x, __uint_as_float(hv[e])));
                         }
+                        store_cols<KC>(taddr + j * 2 * KC, hv);
+                        store_cols<KC>(taddr + j * 2 * KC + KC, lv);
                     }
                     tmem_wait_st();
                     tc_fence_before();
@@ -555,8 +571,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
             }
             asm volatile("bar.sync 2, 128;" ::: "memory");
             for (int cb = kb0 / K2; cb <= (kb1 - 1) / K2; ++cb, ++pseq) {
-                const int pb = pseq & 1;
-                mbar_wait(smem_u32(&bar_pe[pb]), ((pseq >> 1) & 1) ^ 1);
+                const uint32_t pb = pseq % a.npb;
+                mbar_wait(smem_u32(&bar_pe[pb]), ((pseq / a.npb) & 1) ^ 1);
                 const uint32_t buf = sbase + pb * buf_bytes;
                 const int cbase = cb * KC;
                 for (int e = lt; e < E; e += 128) {
@@ -580,26 +596,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                     }
                 }
                 cp_async_wait_all();
-                // split own elements: hi = x with 13 low mantissa bits cleared (exact TF32),
-                // lo = x - hi (exact; the tensor core reads its top 19 bits)
-                for (int e = lt; e < E; e += 128) {
-                    const int j = e >= E1 ? 1 : 0;
-                    const int e1 = e - j * E1;
-                    const int p = e1 / c4n, c4 = e1 - p * c4n;
-                    const uint32_t hi = buf + j * unit_bytes + p * a.pstr + c4 * 16, lo = hi + a.patch_bytes;
-                    float4 v;
-                    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                                 : "r"(hi));
-                    const uint32_t h0 = __float_as_uint(v.x) & 0xffffe000u, h1 = __float_as_uint(v.y) & 0xffffe000u;
-                    const uint32_t h2 = __float_as_uint(v.z) & 0xffffe000u, h3 = __float_as_uint(v.w) & 0xffffe000u;
-                    const float l0 = __fsub_rn(v.x, __uint_as_float(h0)), l1 = __fsub_rn(v.y, __uint_as_float(h1));
-                    const float l2 = __fsub_rn(v.z, __uint_as_float(h2)), l3 = __fsub_rn(v.w, __uint_as_float(h3));
-                    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(hi), "r"(h0), "r"(h1), "r"(h2), "r"(h3)
-                                 : "memory");
-                    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lo), "f"(l0), "f"(l1), "f"(l2), "f"(l3)
-                                 : "memory");
-                }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bar_pf[pb]));
             }
@@ -883,7 +879,11 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     const int PW = p.tpu ? t_out + 2 * p.r : kUX + 2 * p.r, PH = p.tpu ? t_out + 2 * p.r : kUY + 2 * p.r;
     p.patch_px = p.tpu ? p.tpu * PW * PH : PW * PH;
     const unsigned acc = (unsigned)p.umax * p.NBD;
-    const size_t budget = 200 * 1024;
+    size_t budget = kDenseSmemBudget;
+    if (const char* e = getenv("DFX_DENSE_SMEM_KB")) {  // experiments: smaller shared-memory plans
+        const size_t v = (size_t)atoi(e) * 1024;
+        if (v >= 64 * 1024 && v <= 224 * 1024) budget = v;
+    }
     auto set_kc = [&](int kc) {
         p.KC = kc;
         p.nCB = p.cin_pad / p.KC;
@@ -891,11 +891,19 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
         p.patch_bytes = ((unsigned)p.patch_px * p.s_c4 + 127) / 128 * 128;
         p.w_stage = (uint32_t)p.NBD * p.KC * 8;
     };
+    // raw patches (one fp32 plane each) in a ring of npb buffers: the loaders
+    // run up to npb - 1 channel chunks ahead of the A producers
+    p.npb = 2;
     auto fits = [&](int nst, unsigned nbuf) {
-        return 4 * (size_t)p.umax * p.patch_bytes + (size_t)nst * p.w_stage <= budget &&
+        return (size_t)p.npb * p.umax * p.patch_bytes + (size_t)nst * p.w_stage <= budget &&
                nbuf * acc + (unsigned)nst * 2 * p.umax * p.KC <= 512;
     };
     set_kc(p.KC);
+    if (const char* e = getenv("DFX_DENSE_NPB")) {  // experiments: patch ring depth 2..4
+        const int v = atoi(e);
+        if (v >= 2 && v <= kMaxPB) p.npb = v;
+    }
+    if (p.npb > 2 && !fits(4, 2) && !fits(4, 1)) p.npb = 2;
     if (p.KC > 8 && !fits(4, 2) && !fits(4, 1)) set_kc(8);  // large tile-unit patches: 8-channel K-blocks
     // prefer double-buffered accumulators with >= 4 stages, else single with more stages
     p.nbuf = 2;
@@ -907,7 +915,7 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
         while (p.nstw > 2 && !fits(p.nstw, 1)) --p.nstw;
     }
     p.acc_cols = acc;
-    p.smem = 4 * (size_t)p.umax * p.patch_bytes + (size_t)p.nstw * p.w_stage;
+    p.smem = (size_t)p.npb * p.umax * p.patch_bytes + (size_t)p.nstw * p.w_stage;
     const int BH = t_out > kUY ? t_out : kUY, BW = t_out > kUX ? t_out : kUX;
     p.ok = fits(p.nstw, p.nbuf) && k * k <= 49 && (k & 1) && t_out <= 64 && (BH / kUY) * (BW / kUX) <= 32 &&
            (BH / t_out) * (BW / t_out) <= 32 && p.patch_px * p.umax <= 2 * 22 * 14;
@@ -973,7 +981,7 @@ template <int KC>
 static void launch_kc(int grid, size_t smem, cudaStream_t s, const Ctx& c, const DenseArgs& a) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_conv_dense<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_conv_dense<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
         configured = true;
     }
     launch_pdl(k_conv_dense<KC>, grid, kDenseThreads, smem, s, c, a);
@@ -986,7 +994,8 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
     if (!p.ok) throw std::runtime_error("conv_dense: unsupported layer shape");
     DenseArgs a{in, out, w, units, nunits, p.smax > 1 ? ws : nullptr, cnt, cin, cout, p.cout_pad, p.k, p.r,
                 p.KC, p.nCB, p.NBD, p.nNB, p.nstw, p.smax > 1 ? p.smax : 1, num_sms, p.s_c4, p.patch_bytes,
-                p.w_stage, p.acc_cols, p.nbuf, p.nbuf * p.acc_cols, p.umax, p.tpu, p.tsh, p.patch_px, nullptr, 0};
+                p.w_stage, p.acc_cols, p.nbuf, p.nbuf * p.acc_cols, p.umax, p.tpu, p.tsh, p.patch_px, p.npb, nullptr,
+                0};
     if (getenv("DFX_CONV_DBG") && !g_trace) cudaMalloc(&g_trace, 1024 * 8);
     a.trace = g_trace;
     if (const char* d = getenv("DFX_CONV_DBG")) a.dbg = atoi(d);

@@ -99,6 +99,7 @@ struct DenseConvPlan {
     int tpu;     // tile units: tiles of T x T px per 128-row unit (T = t_out in {2, 4, 8}); 0 = 16x8-px units
     int tsh;     // log2(t_out) in tile-unit mode
     int patch_px;
+    int npb;       // patch ring depth
     int ws_units;  // max 128-row units of a frame (split-K workspace rows / 128)
     unsigned s_c4, patch_bytes, w_stage, acc_cols, nbuf;
     size_t smem;
