@@ -713,7 +713,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
         // lane issues the MMAs and commits. Both units use the same weight stage.
         const uint32_t idesc = idesc_tf32(a.NBD);
         const uint32_t lbo_b = (uint32_t)a.NBD * 16, half_w = a.w_stage / 2;
-        uint32_t st = 0, ph = 0, ui = 0;
+        uint32_t st = 0, ph = 0, ui = 0, tq = 0;
+        const bool trc = (a.dbg & 64) && blockIdx.x == 0;
         for (int it = blockIdx.x; it < items; it += gridDim.x, ++ui) {
             int pr, nb, kb0, kb1;
             item_info(it, pr, nb, kb0, kb1);
@@ -729,8 +730,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                 const bool two = kb + 1 < kb1;
                 const uint32_t st1 = st + 1 == (uint32_t)NST ? 0 : st + 1;
                 const uint32_t ph1 = st + 1 == (uint32_t)NST ? ph ^ 1 : ph;
+                const long long m_a = trc ? clock64() : 0;
                 mbar_wait(smem_u32(&bar_full[st]), ph);
                 if (two) mbar_wait(smem_u32(&bar_full[st1]), ph1);
+                const long long m_b = trc ? clock64() : 0;
                 tc_fence_after();
                 if (elect_one()) {
 #pragma unroll 1
@@ -756,6 +759,12 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                     }
                 }
                 __syncwarp();
+                if (trc && lane == 0 && tq < 100) {  // microbenchmark stamps (dbg & 64)
+                    a.trace[600 + 3 * tq] = m_a;
+                    a.trace[601 + 3 * tq] = m_b;
+                    a.trace[602 + 3 * tq] = clock64();
+                    ++tq;
+                }
                 if (two) {
                     st = st1 + 1 == (uint32_t)NST ? 0 : st1 + 1;
                     ph = st1 + 1 == (uint32_t)NST ? ph1 ^ 1 : ph1;
@@ -999,6 +1008,10 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
     if (getenv("DFX_CONV_DBG") && !g_trace) cudaMalloc(&g_trace, 1024 * 8);
     a.trace = g_trace;
     if (const char* d = getenv("DFX_CONV_DBG")) a.dbg = atoi(d);
+    if (const char* d = getenv("DFX_CONV_TRACE_IDX")) {  // trace only the i-th dense launch of every 8
+        static int seq = 0;
+        if (seq++ % 8 != atoi(d)) a.dbg &= ~64;
+    }
     DenseConvPlan pp = p;
     if (a.dbg & 128) a.smax = 1;  // microbenchmark: no split-K
     if (const char* d = getenv("DFX_CONV_NST")) {  // microbenchmark: fewer pipeline stages
