@@ -127,17 +127,32 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Floor division by a runtime divisor: an arithmetic shift (exact floor for
+// negative values too) when the divisor is a power of two, which every tile
+// size and block width of a network with pow2 tiles is.
+struct FDiv {
+    int d, sh;
+    __device__ __forceinline__ explicit FDiv(int v) : d(v), sh(-1) {
+        if (v > 0 && (v & (v - 1)) == 0) {
+            sh = 0;
+            while ((1 << sh) < v) ++sh;
+        }
+    }
+    __device__ __forceinline__ int operator()(int x) const { return sh >= 0 ? (x >> sh) : floor_div32(x, d); }
+};
+
 __device__ __forceinline__ bool pkt_ok(const PktDev& p, int th, int tw, int y, int x) {
     if (y < -p.halo || y >= th * p.t + p.halo || x < -p.halo || x >= tw * p.t + p.halo) return false;
     return p.ext[ext_idx(p, floor_div32(y, p.t), floor_div32(x, p.t))] != 0;
 }
 
 // Target test of a stride-1 window (delta_layers.cpp:34-45, :60-70).
-__device__ __forceinline__ bool is_target_s1(const PktDev& in, int th, int tw, int oy, int ox, int k, int r) {
+__device__ __forceinline__ bool is_target_s1(const PktDev& in, int th, int tw, int oy, int ox, int k, int r,
+                                             const FDiv& dt) {
     const int iy0 = oy - r - in.halo, iy1 = oy - r + k - 1 + in.halo;
     const int ix0 = ox - r - in.halo, ix1 = ox - r + k - 1 + in.halo;
-    const int tr0 = max(floor_div32(iy0, in.t), 0), tr1 = min(floor_div32(iy1, in.t), th - 1);
-    const int tc0 = max(floor_div32(ix0, in.t), 0), tc1 = min(floor_div32(ix1, in.t), tw - 1);
+    const int tr0 = max(dt(iy0), 0), tr1 = min(dt(iy1), th - 1);
+    const int tc0 = max(dt(ix0), 0), tc1 = min(dt(ix1), tw - 1);
     for (int tr = tr0; tr <= tr1; ++tr)
         for (int tc = tc0; tc <= tc1; ++tc)
             if (in.ext[ext_idx(in, tr, tc)]) return true;
@@ -178,6 +193,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
     if (Y0 >= eh + hg || X0 >= ew + hg || Y0 + BH <= -hg || X0 + BW <= -hg) return;
     const int upr = BW / kUX, nun = (BH / kUY) * upr;  // units in block
     const int tpr = BW / t, ntl = (BH / t) * tpr;        // tiles in block
+    const FDiv dbw(BW), dt(t), din(in.t), dtpr(tpr);
     if (threadIdx.x < 32) {
         s_ucnt[threadIdx.x] = 0;
         s_tstore[threadIdx.x] = 0;
@@ -190,13 +206,13 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
         bool tgt = false;
         int uid = -1;
         if (p < npx) {
-            const int ly = p / BW, lx = p - (p / BW) * BW;
+            const int ly = dbw(p), lx = p - ly * BW;
             const int y = Y0 + ly, x = X0 + lx;
-            if (y >= -hg && y < eh + hg && x >= -hg && x < ew + hg) tgt = is_target_s1(in, F.th, F.tw, y, x, k, r);
+            if (y >= -hg && y < eh + hg && x >= -hg && x < ew + hg) tgt = is_target_s1(in, F.th, F.tw, y, x, k, r, din);
             if (tgt) {
                 ++geo;
                 uid = (ly / kUY) * upr + lx / kUX;
-                if (y >= -hs && y < eh + hs && x >= -hs && x < ew + hs) s_tstore[(ly / t) * tpr + lx / t] = 1;
+                if (y >= -hs && y < eh + hs && x >= -hs && x < ew + hs) s_tstore[dt(ly) * tpr + dt(lx)] = 1;
             }
         }
         // per-unit target counts, aggregated per warp (one shared atomic per unit and warp)
@@ -226,7 +242,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
             bool g = false;
             int y = 0, x = 0;
             if (p < npx && ((s_bits[p >> 5] >> (p & 31)) & 1u)) {
-                const int ly = p / BW, lx = p - (p / BW) * BW;
+                const int ly = dbw(p), lx = p - ly * BW;
                 y = Y0 + ly, x = X0 + lx;
                 g = s_ucnt[(ly / kUY) * upr + lx / kUX] < tau && y >= -hs && y < eh + hs && x >= -hs && x < ew + hs;
             }
@@ -238,7 +254,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
         }
     }
     if (threadIdx.x < ntl) {
-        const int ti = floor_div32(Y0, t) + threadIdx.x / tpr, tj = floor_div32(X0, t) + threadIdx.x % tpr;
+        const int ti = dt(Y0) + dtpr((int)threadIdx.x), tj = dt(X0) + (int)threadIdx.x - dtpr((int)threadIdx.x) * tpr;
         if (ti >= -out.RT && ti < F.th + out.RT && tj >= -out.RT && tj < F.tw + out.RT) {
             out.ext[ext_idx(out, ti, tj)] = s_tstore[threadIdx.x] ? 1 : 0;
             if (tile_units && s_tstore[threadIdx.x]) units[atomicAdd(nunits, 1)] = ((ti + 8) << 16) | (tj + 8);
@@ -249,11 +265,12 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
     const bool active_tile = __syncthreads_or(threadIdx.x < ntl && s_tstore[threadIdx.x]);
     if ((nun > 1 || tau > 1) && sparse_unit && active_tile) {
         const int C = out.C;
-        for (int e = threadIdx.x; e < npx * ((C & 3) == 0 ? C / 4 : C); e += kPlanThreads) {
-            const int per = (C & 3) == 0 ? C / 4 : C;
-            const int p = e / per, q = e - p * per;
-            const int ly = p / BW, lx = p - (p / BW) * BW;
-            if (s_ucnt[(ly / kUY) * upr + lx / kUX] >= tau || !s_tstore[(ly / t) * tpr + lx / t] ||
+        const int per = (C & 3) == 0 ? C / 4 : C;
+        const FDiv dper(per);
+        for (int e = threadIdx.x; e < npx * per; e += kPlanThreads) {
+            const int p = dper(e), q = e - p * per;
+            const int ly = dbw(p), lx = p - ly * BW;
+            if (s_ucnt[(ly / kUY) * upr + lx / kUX] >= tau || !s_tstore[dt(ly) * tpr + dt(lx)] ||
                 ((s_bits[p >> 5] >> (p & 31)) & 1u))
                 continue;
             const int y = Y0 + ly, x = X0 + lx;
