@@ -301,6 +301,7 @@ struct DenseArgs {
     int tpu, tsh;          // tile-unit mode (tpu tiles of 2^tsh px per unit), tpu = 0: 16x8-px units
     int ppx;               // pixels of one unit's patch
     int npb;               // patch ring depth (raw fp32 patches; the producers split hi / lo)
+    int nmma;              // MMA issuer warps (2: K-block pairs alternate, one accumulator each)
     long long* trace;      // microbenchmark (dbg & 64): per-K-block clock64 stamps of CTA 0
     int dbg;               // microbenchmark knobs (tools/bench_conv.cu): 1 no MMA, 2 no patch, 4 no weights
 };
@@ -364,7 +365,7 @@ constexpr int kMaxPB = 4;  // patch ring depth limit
 #define DFX_DENSE_SMEM_KB 200
 #endif
 constexpr size_t kDenseSmemBudget = (size_t)DFX_DENSE_SMEM_KB * 1024;
-constexpr int kDenseThreads = (4 * kProdWG + 10) * 32;
+constexpr int kDenseThreads = (4 * kProdWG + 11) * 32;  // + loaders, epilogue, 2 MMA issuers, weights
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
     asm volatile(
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     const int PW = a.tpu ? (1 << a.tsh) + 2 * a.r : kUX + 2 * a.r;  // patch row pitch (pixels)
     const int NST = a.nst;
     // TMEM: accumulators [nbuf][2 units][NBD] then NST A stages of [2 units][hi KC | lo KC]
-    const uint32_t acc_buf = a.umax * a.NBD;
+    const uint32_t acc_buf = a.nmma * a.umax * a.NBD;  // [nmma issuers][umax units][NBD]
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
             mbar_init(smem_u32(&bar_pe[i]), 4 * kProdWG);
         }
         for (int i = 0; i < 2; ++i) {
-            mbar_init(smem_u32(&bar_af[i]), 1);
+            mbar_init(smem_u32(&bar_af[i]), a.nmma);
             mbar_init(smem_u32(&bar_ae[i]), 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -646,9 +647,16 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                     dst_row = a.out.d + pkt_off(a.out, y, x);
                 }
                 const uint32_t tcol = tmem + b * acc_buf + j * a.NBD + ((uint32_t)(q * 32) << 16);
+                const bool two_acc = a.nmma == 2 && kb1 - kb0 > 2;  // the second issuer had K-blocks
                 for (int cc = 0; cc < a.NBD; cc += 32) {
                     float v[32];
                     tmem_ld32(tcol + (uint32_t)cc, v);
+                    if (two_acc) {  // fixed order: issuer 0 partial + issuer 1 partial
+                        float v1[32];
+                        tmem_ld32(tcol + (uint32_t)(a.umax * a.NBD) + (uint32_t)cc, v1);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(v[i], v1[i]);
+                    }
                     const int o0 = nb * a.NBD + cc;
                     if (dst_row) {
                         float* dst = dst_row + o0;
@@ -724,10 +732,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                 a.trace[505 + 2 * ui] = clock64();
             }
         }
-    } else if (warp == 4 * kProdWG + 8) {
-        // ------------------------------------------------ MMA issuer
+    } else if (warp == 4 * kProdWG + 8 || (warp == 4 * kProdWG + 10 && a.nmma == 2)) {
+        // ------------------------------------------------ MMA issuers
         // Warp-uniform loop (descriptors in uniform registers); one elected
         // lane issues the MMAs and commits. Both units use the same weight stage.
+        // With two issuers, K-block pairs alternate between them, each into its
+        // own accumulator (summed in fixed order by the epilogue): one issuer's
+        // barrier waits overlap the other's MMAs, so the tensor pipe stays fed.
+        const int mw = warp == 4 * kProdWG + 8 ? 0 : 1;
         const uint32_t idesc = idesc_tf32(a.NBD);
         const uint32_t lbo_b = (uint32_t)a.NBD * 16, half_w = a.w_stage / 2;
         uint32_t st = 0, ph = 0, ui = 0, tq = 0;
@@ -739,14 +751,23 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
             const uint32_t b = a.nbuf == 2 ? (ui & 1) : 0, ub = a.nbuf == 2 ? (ui >> 1) : ui;
             mbar_wait(smem_u32(&bar_ae[b]), (ub & 1) ^ 1);
             tc_fence_after();
-            const uint32_t dtm = tmem + b * acc_buf;
+            const uint32_t dtm = tmem + b * acc_buf + mw * a.umax * a.NBD;
             // two K-blocks per handshake: wait for both stages, issue both MMA
             // chains back to back (the per-K-block wait/fence overhead is
             // otherwise a bubble in the tensor pipe)
-            for (int kb = kb0; kb < kb1; kb += 2) {
+            for (int kb = kb0, q = 0; kb < kb1; kb += 2, ++q) {
                 const bool two = kb + 1 < kb1;
                 const uint32_t st1 = st + 1 == (uint32_t)NST ? 0 : st + 1;
                 const uint32_t ph1 = st + 1 == (uint32_t)NST ? ph ^ 1 : ph;
+                if (q % a.nmma != mw) {  // the other issuer's pair: advance the ring only
+                    if (two) {
+                        st = st1 + 1 == (uint32_t)NST ? 0 : st1 + 1;
+                        ph = st1 + 1 == (uint32_t)NST ? ph1 ^ 1 : ph1;
+                    } else {
+                        st = st1, ph = ph1;
+                    }
+                    continue;
+                }
                 const long long m_a = trc ? clock64() : 0;
                 mbar_wait(smem_u32(&bar_full[st]), ph);
                 if (two) mbar_wait(smem_u32(&bar_full[st1]), ph1);
@@ -763,7 +784,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                             for (int j = 0; j < KC / 8; ++j) {
                                 const uint64_t dbh = umma_desc(wb + 2 * j * lbo_b, lbo_b, 128);
                                 const uint64_t dbl = umma_desc(wb + half_w + 2 * j * lbo_b, lbo_b, 128);
-                                const uint32_t acc = (kb + h > kb0 || j > 0) ? 1u : 0u;
+                                const uint32_t acc = (q > mw || h > 0 || j > 0) ? 1u : 0u;
                                 for (int uu = 0; uu < nu; ++uu) {
                                     const uint32_t d = dtm + uu * a.NBD, at = a_tm + uu * 2 * KC;
                                     mma_tf32_ts(d, at + KC + 8 * j, dbh, idesc, acc);
@@ -776,7 +797,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                     }
                 }
                 __syncwarp();
-                if (trc && lane == 0 && tq < 100) {  // microbenchmark stamps (dbg & 64)
+                if (trc && mw == 0 && lane == 0 && tq < 100) {  // microbenchmark stamps (dbg & 64)
                     a.trace[600 + 3 * tq] = m_a;
                     a.trace[601 + 3 * tq] = m_b;
                     a.trace[602 + 3 * tq] = clock64();
@@ -792,7 +813,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
             if (elect_one()) mma_commit(smem_u32(&bar_af[b]));
             __syncwarp();
         }
-    } else {
+    } else if (warp == 4 * kProdWG + 9) {
         // ------------------------------------------------ weight producer
         if (lane == 0) {
             uint32_t st = 0, ph = 0;
@@ -920,9 +941,10 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     // raw patches (one fp32 plane each) in a ring of npb buffers: the loaders
     // run up to npb - 1 channel chunks ahead of the A producers
     p.npb = 2;
+    p.nmma = 1;
     auto fits = [&](int nst, unsigned nbuf) {
         return (size_t)p.npb * p.umax * p.patch_bytes + (size_t)nst * p.w_stage <= budget &&
-               nbuf * acc + (unsigned)nst * 2 * p.umax * p.KC <= 512;
+               nbuf * acc * p.nmma + (unsigned)nst * 2 * p.umax * p.KC <= 512;
     };
     set_kc(p.KC);
     if (const char* e = getenv("DFX_DENSE_NPB")) {  // experiments: patch ring depth 2..4
@@ -931,6 +953,13 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     }
     if (p.npb > 2 && !fits(4, 2) && !fits(4, 1)) p.npb = 2;
     if (p.KC > 8 && !fits(4, 2) && !fits(4, 1)) set_kc(8);  // large tile-unit patches: 8-channel K-blocks
+    // two MMA issuers (one accumulator each) when TMEM holds them with >= 4 stages
+    {
+        int want = 2;
+        if (const char* e = getenv("DFX_DENSE_NMMA")) want = atoi(e) == 1 ? 1 : 2;
+        p.nmma = want;
+        if (!fits(4, 2) && !fits(4, 1)) p.nmma = 1;
+    }
     // prefer double-buffered accumulators with >= 4 stages, else single with more stages
     p.nbuf = 2;
     p.nstw = 8;
@@ -940,7 +969,7 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
         p.nstw = 8;
         while (p.nstw > 2 && !fits(p.nstw, 1)) --p.nstw;
     }
-    p.acc_cols = acc;
+    p.acc_cols = acc * p.nmma;
     p.smem = (size_t)p.npb * p.umax * p.patch_bytes + (size_t)p.nstw * p.w_stage;
     const int BH = t_out > kUY ? t_out : kUY, BW = t_out > kUX ? t_out : kUX;
     p.ok = fits(p.nstw, p.nbuf) && k * k <= 49 && (k & 1) && t_out <= 64 && (BH / kUY) * (BW / kUX) <= 32 &&
@@ -1020,8 +1049,8 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
     if (!p.ok) throw std::runtime_error("conv_dense: unsupported layer shape");
     DenseArgs a{in, out, w, units, nunits, p.smax > 1 ? ws : nullptr, cnt, cin, cout, p.cout_pad, p.k, p.r,
                 p.KC, p.nCB, p.NBD, p.nNB, p.nstw, p.smax > 1 ? p.smax : 1, num_sms, p.s_c4, p.patch_bytes,
-                p.w_stage, p.acc_cols, p.nbuf, p.nbuf * p.acc_cols, p.umax, p.tpu, p.tsh, p.patch_px, p.npb, nullptr,
-                0};
+                p.w_stage, p.acc_cols, p.nbuf, p.nbuf * p.acc_cols, p.umax, p.tpu, p.tsh, p.patch_px, p.npb,
+                p.nmma, nullptr, 0};
     if (getenv("DFX_CONV_DBG") && !g_trace) cudaMalloc(&g_trace, 1024 * 8);
     a.trace = g_trace;
     if (const char* d = getenv("DFX_CONV_DBG")) a.dbg = atoi(d);

@@ -100,6 +100,7 @@ struct DenseConvPlan {
     int tsh;     // log2(t_out) in tile-unit mode
     int patch_px;
     int npb;       // patch ring depth
+    int nmma;      // MMA issuer warps (1 or 2)
     int ws_units;  // max 128-row units of a frame (split-K workspace rows / 128)
     unsigned s_c4, patch_bytes, w_stage, acc_cols, nbuf;
     size_t smem;
