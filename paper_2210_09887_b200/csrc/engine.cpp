@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <memory>
 #include <string>
@@ -196,6 +197,14 @@ class Engine {
     void ensure_staging(int c, int h, int w, bool host_frame);
     PktDev in_packet(int idx) const { return idx == -1 ? in_pkt_ : lrt_[idx].pkt; }
     Ctx ctx() const { return Ctx{d_frame_, d_slots_, rows_, cols_, d_own_}; }
+    void set_param_slot(int i) {
+        uint8_t* b = params_d_.p + (size_t)i * pstride_;
+        d_frame_ = reinterpret_cast<FrameDev*>(b);
+        d_slots_ = reinterpret_cast<SlotDev*>(b + off_slots_);
+        d_claims_ = reinterpret_cast<int*>(b + off_claims_);
+        d_fresh_ = b + off_fresh_;
+        d_own_ = b + off_own_;
+    }
 
     Net net_;
     dfx_engine_config cfg_;
@@ -223,6 +232,12 @@ class Engine {
     uint8_t* params_hb_[2] = {nullptr, nullptr};
     cudaEvent_t params_ev_[2] = {nullptr, nullptr};
     int pslot_ = 0;
+    uint8_t* params_hd_[2] = {nullptr, nullptr};  // device views of the mapped host blocks
+    size_t pstride_ = 0;                           // params slot stride (16-byte multiple)
+    unsigned* ack_h_ = nullptr;                    // mapped: last frame whose block k_frame_begin consumed
+    unsigned* ack_d_ = nullptr;
+    unsigned fseq_ = 0, pslot_seq_[2] = {0, 0};
+    uint8_t* readback_d_ = nullptr;                // device view of readback_h_
     size_t params_bytes_ = 0, off_slots_ = 0, off_claims_ = 0, off_fresh_ = 0, off_own_ = 0;
     FrameDev* d_frame_ = nullptr;
     SlotDev* d_slots_ = nullptr;
@@ -296,8 +311,10 @@ Engine::~Engine() {
     for (int i = 0; i < 2; ++i) {
         if (params_hb_[i]) cudaFreeHost(params_hb_[i]);
         if (params_ev_[i]) cudaEventDestroy(params_ev_[i]);
+        params_hb_[i] = nullptr;
     }
     if (readback_h_) cudaFreeHost(readback_h_);
+    if (ack_h_) cudaFreeHost(ack_h_);
     if (in_h_) cudaFreeHost(in_h_);
     if (out_h_) cudaFreeHost(out_h_);
     if (cstream_) cudaStreamSynchronize(cstream_);
@@ -490,17 +507,22 @@ void Engine::allocate(int th, int tw) {
     off_fresh_ = off_claims_ + (size_t)max_claims_ * sizeof(int);
     off_own_ = off_fresh_ + slots;
     params_bytes_ = off_own_ + slots;
-    params_d_.alloc(params_bytes_);
+    // two device slots (alternating per frame) filled by k_frame_begin from two
+    // mapped page-locked host blocks
+    pstride_ = (params_bytes_ + 255) / 256 * 256;
+    params_d_.alloc(2 * pstride_);
     for (int i = 0; i < 2; ++i) {
-        CUDA_CHECK(cudaMallocHost(&params_hb_[i], params_bytes_));
-        memset(params_hb_[i], 0, params_bytes_);
+        CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&params_hb_[i]), pstride_, cudaHostAllocMapped));
+        memset(params_hb_[i], 0, pstride_);
+        CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&params_hd_[i]), params_hb_[i], 0));
         CUDA_CHECK(cudaEventCreateWithFlags(&params_ev_[i], cudaEventDisableTiming));
     }
-    d_frame_ = reinterpret_cast<FrameDev*>(params_d_.p);
-    d_slots_ = reinterpret_cast<SlotDev*>(params_d_.p + off_slots_);
-    d_claims_ = reinterpret_cast<int*>(params_d_.p + off_claims_);
-    d_fresh_ = params_d_.p + off_fresh_;
-    d_own_ = params_d_.p + off_own_;
+    CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&ack_h_), 64, cudaHostAllocMapped));
+    *reinterpret_cast<volatile unsigned*>(ack_h_) = 0;
+    CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ack_d_), ack_h_, 0));
+    fseq_ = 0;
+    pslot_seq_[0] = pslot_seq_[1] = 0;
+    set_param_slot(0);
 
     const size_t nl = net_.layers.size();
     off_dropped_ = nl * 8;
@@ -508,9 +530,11 @@ void Engine::allocate(int th, int tw) {
     off_ucounts_ = off_counts_ + nl * 4;
     off_gbar_ = off_ucounts_ + nl * 4;
     off_tmax_ = (off_gbar_ + nl * 4 + 15) / 16 * 16;
-    cnt_bytes_ = off_tmax_ + nl * (size_t)slots * 4;
+    cnt_bytes_ = (off_tmax_ + nl * (size_t)slots * 4 + 15) / 16 * 16;
     counters_d_.alloc(cnt_bytes_);
-    CUDA_CHECK(cudaMallocHost(&readback_h_, nl * 8 + 8 + slots));
+    CUDA_CHECK(cudaMemset(counters_d_.p, 0, cnt_bytes_));
+    CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&readback_h_), nl * 8 + 8 + slots, cudaHostAllocMapped));
+    CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&readback_d_), readback_h_, 0));
 
     const int ot = net_.layers[net_.out_layer].in_tile;
     out_d_.alloc((size_t)net_.layers[net_.out_layer].in_channels * rows_ * ot * cols_ * ot);
@@ -631,7 +655,9 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     // the pinned block this frame writes may still feed an in-flight upload
     pslot_ ^= 1;
     uint8_t* params_h_ = params_hb_[pslot_];
-    CUDA_CHECK(cudaEventSynchronize(params_ev_[pslot_]));
+    // the host block is free once k_frame_begin of the slot's previous frame consumed it
+    while (*reinterpret_cast<volatile unsigned*>(ack_h_) < pslot_seq_[pslot_]) {
+    }
     memcpy(params_h_, &F, sizeof F);
     SlotDev* hs = reinterpret_cast<SlotDev*>(params_h_ + off_slots_);
     const auto& slots = ledger_.slots();
@@ -653,10 +679,13 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
             const auto& sl = slots[ledger_.slot_index(t)];
             ho[r * tw + cc] = (sl.used && sl.coord.tx == t.tx && sl.coord.ty == t.ty) ? 1 : 0;
         }
-    CUDA_CHECK(cudaMemcpyAsync(params_d_.p, params_h_, params_bytes_, cudaMemcpyHostToDevice, stream_));
-    CUDA_CHECK(cudaEventRecord(params_ev_[pslot_], stream_));
-    CUDA_CHECK(cudaMemsetAsync(counters_d_.p, 0, cnt_bytes_, stream_));
+    pslot_seq_[pslot_] = ++fseq_;
+    set_param_slot(pslot_);
+    std::atomic_thread_fence(std::memory_order_release);
     launches_ = 0;
+    launch_frame_begin(stream_, params_hd_[pslot_], params_d_.p + (size_t)pslot_ * pstride_, pstride_, counters_d_.p,
+                       cnt_bytes_, ack_d_, fseq_);
+    ++launches_;
     const Ctx C = ctx();
     cudaStream_t s = stream_;
     auto* flop_px = reinterpret_cast<unsigned long long*>(counters_d_.p);
@@ -770,13 +799,12 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
         }
     }
     const LayerRT& ort = lrt_[net_.out_layer];
-    PROF(DFX_FAM_DENSIFY, launch_densify(C, s, ort.acc, ort.aux, out_cur_ ? out_cur_ : out_d_.p));
+    const Readback rb{counters_d_.p, (int)(net_.layers.size() * 8 + 8), in_pkt_ext_.p, rows_ * cols_, readback_d_};
+    PROF(DFX_FAM_DENSIFY, launch_densify(C, s, ort.acc, ort.aux, out_cur_ ? out_cur_ : out_d_.p, rb));
     CUDA_CHECK(cudaGetLastError());
 
-    // small readback: per-layer target counts, dropped, fired input tiles
-    const size_t nl = net_.layers.size();
-    CUDA_CHECK(cudaMemcpyAsync(readback_h_, counters_d_.p, nl * 8 + 8, cudaMemcpyDeviceToHost, s));
-    CUDA_CHECK(cudaMemcpyAsync(readback_h_ + nl * 8 + 8, in_pkt_ext_.p, (size_t)rows_ * cols_, cudaMemcpyDeviceToHost, s));
+    // the small readback (per-layer target counts, dropped, fired input tiles) is
+    // written into mapped host memory by the last kernel (launch_densify)
     place_ = pl;
     const Layer& ol = net_.layers[net_.out_layer];
     info.out_channels = ol.in_channels;
@@ -1363,6 +1391,10 @@ int dfx_debug_conv_trace(long long* out, int n) {
         dfx::check(cudaMemcpy(out, t, (size_t)(n < 1024 ? n : 1024) * 8, cudaMemcpyDeviceToHost) == cudaSuccess,
                    "trace copy failed");
     });
+}
+// Debug: frame-boundary stamps (DFX_FRAME_TRACE=1), [64][4] u64.
+int dfx_debug_frame_trace(unsigned long long* out) {
+    return guard([&] { memcpy(out, dfx::frame_trace_host(), 64 * 4 * 8); });
 }
 // Debug: truncation phase stamps (DFX_TRUNC_TRACE=1), [64][1024][8] u64.
 int dfx_debug_trunc_trace(unsigned long long* out, long long n) {

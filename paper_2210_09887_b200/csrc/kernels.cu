@@ -367,8 +367,49 @@ __global__ void k_input_apply(Ctx c, const float* __restrict__ aligned, const ui
 // Claimed tiles of every buffer: zero, or the bias-init fill for truncated
 // buffers (buffer_manager.cpp:68-89, engine.cpp:78-91; fill after zero == fill).
 // Persistent grid-stride over (buffer, claim, element) with 16-byte stores.
-__global__ void k_claims(Ctx c, const int* __restrict__ claim_slots, const ClaimBuf* __restrict__ bufs, int nbuf) {
+// First kernel of every frame: the frame's parameter block is read straight
+// from page-locked (mapped) host memory into its device slot, the frame's
+// counters are zeroed, and the host is told the host block may be reused. No
+// copy / memset node sits in the engine stream, so frames chain through
+// programmatic dependent launch end to end. The parameter slot alternates per
+// frame: the copy runs BEFORE the dependency wait, overlapping the previous
+// frame's last kernel, which reads the other slot.
+__device__ unsigned g_begin_done;
+__global__ void k_frame_begin(const uint4* __restrict__ src, uint4* __restrict__ dst, int n16,
+                              uint4* __restrict__ counters, int cnt16, volatile unsigned* ack, unsigned seq) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    for (int i = tid; i < n16; i += nth) dst[i] = src[i];
     pdl_enter();
+    for (int i = tid; i < cnt16; i += nth) counters[i] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&g_begin_done, 1u) == gridDim.x - 1) {  // every CTA has read its part of the host block
+            g_begin_done = 0;
+            __threadfence_system();
+            *ack = seq;
+        }
+    }
+}
+
+// Frame-boundary trace (DFX_FRAME_TRACE=1, development only): [64 frames][4]
+// globaltimer stamps: claims entry, claims past its dependency wait, densify end.
+__device__ unsigned long long g_fstamp[64 * 4];
+__device__ unsigned g_fseq;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__global__ void k_claims(Ctx c, const int* __restrict__ claim_slots, const ClaimBuf* __restrict__ bufs, int nbuf,
+                         int trace) {
+    const unsigned long long t0 = trace ? gtimer() : 0;
+    pdl_enter();
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned s = atomicAdd(&g_fseq, 1u) % 64;
+        g_fstamp[s * 4 + 0] = t0;
+        g_fstamp[s * 4 + 1] = gtimer();
+    }
     const FrameDev& F = *c.f;
     const int nq = F.nclaims;
     const long long tid0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, nthr = (long long)gridDim.x * blockDim.x;
@@ -1096,8 +1137,16 @@ __global__ void k_add(Ctx c, PktDev a, PktDev b, PktDev out) {
 // Output = acc + trunc over the placement, CHW (delta_layers.cpp:395-400).
 // C % 8 == 0: a warp takes (8-channel group, output row); each lane one pixel:
 // 2 x 16-B reads of acc and trunc, 8 plane writes coalesced across the warp.
-__global__ void k_densify8(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ out) {
+// The frame's small readback (per-layer counts, dropped pixels, fired input
+// tiles) written by CTA 0 of the last kernel straight into mapped host memory.
+__device__ __forceinline__ void frame_readback(const Readback& rb) {
+    if (blockIdx.x != 0 || !rb.dst) return;
+    for (int i = threadIdx.x; i < rb.n1; i += blockDim.x) rb.dst[i] = rb.src1[i];
+    for (int i = threadIdx.x; i < rb.n2; i += blockDim.x) rb.dst[rb.n1 + i] = rb.src2[i];
+}
+__global__ void k_densify8(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ out, int trace, Readback rb) {
     pdl_enter();
+    frame_readback(rb);
     const FrameDev& F = *c.f;
     const int t = acc.t, C = acc.C, G = C / 8;
     const int oh = F.th * t, ow = F.tw * t;
@@ -1126,10 +1175,18 @@ __global__ void k_densify8(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ 
             o[7 * plane] = __fadd_rn(a1.w, t1.w);
         }
     }
+    if (trace) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned s = (atomicAdd(&g_fseq, 0u) + 63) % 64;
+            atomicMax(&g_fstamp[s * 4 + 2], gtimer());
+        }
+    }
 }
 
-__global__ void k_densify(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ out) {
+__global__ void k_densify(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ out, Readback rb) {
     pdl_enter();
+    frame_readback(rb);
     const FrameDev& F = *c.f;
     const int t = acc.t, C = acc.C;
     const int oh = F.th * t, ow = F.tw * t;
@@ -1165,6 +1222,12 @@ static int persistent_grid(long long work) {
     return g < 1 ? 1 : (int)g;
 }
 
+unsigned long long* frame_trace_host() {
+    static unsigned long long h[64 * 4];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, g_fstamp, sizeof h);
+    return h;
+}
 void launch_warp(const Ctx& c, cudaStream_t s, const float* frame, int C, float* warped, uint8_t* fp) {
     // frame dims are per-frame but bounded by the staging buffer; use a persistent grid
     launch_pdl(k_warp, num_sms_cached() * 8, kThreads, 0, s, c, frame, C, warped, fp);
@@ -1205,7 +1268,8 @@ void launch_input_apply(const Ctx& c, cudaStream_t s, const float* aligned, cons
 void launch_claims(const Ctx& c, cudaStream_t s, const int* claim_slots, const ClaimBuf* bufs, int nbuf,
                    int max_claims) {
     if (nbuf <= 0 || max_claims <= 0) return;
-    launch_pdl(k_claims, num_sms_cached() * 8, kThreads, 0, s, c, claim_slots, bufs, nbuf);
+    static const int trace = getenv("DFX_FRAME_TRACE") ? 1 : 0;
+    launch_pdl(k_claims, num_sms_cached() * 8, kThreads, 0, s, c, claim_slots, bufs, nbuf, trace);
 }
 void launch_ring_add(const Ctx& c, cudaStream_t s, PktDev in, BufDev dst) {
     if (in.halo <= 0) return;
@@ -1286,13 +1350,20 @@ void launch_conv_exact(const Ctx& c, cudaStream_t s, PktDev in, const float* w, 
     if (g < 1) g = 1;
     launch_pdl(k_conv_exact, (int)g, 256, smem, s, c, in, w, cin, cout, k, st, r, out, hg, list, count, ci);
 }
-void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out) {
+void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out, Readback rb) {
     if ((acc.C & 7) == 0) {
-        launch_pdl(k_densify8, num_sms_cached() * 8, kThreads, 0, s, c, acc, trunc, out);
+        static const int trace = getenv("DFX_FRAME_TRACE") ? 1 : 0;
+        launch_pdl(k_densify8, num_sms_cached() * 8, kThreads, 0, s, c, acc, trunc, out, trace, rb);
         return;
     }
     launch_pdl(k_densify, persistent_grid((long long)acc.C * c.rows * acc.t * c.cols * acc.t), kThreads, 0, s, c, acc, trunc,
-                                                                                                       out);
+               out, rb);
+}
+void launch_frame_begin(cudaStream_t s, const void* src, void* dst, size_t bytes, void* counters, size_t cnt_bytes,
+                        unsigned* ack, unsigned seq) {
+    launch_pdl(k_frame_begin, 32, kThreads, 0, s, reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst),
+               (int)(bytes / 16), reinterpret_cast<uint4*>(counters), (int)(cnt_bytes / 16), (volatile unsigned*)ack,
+               seq);
 }
 
 }  // namespace dfx

@@ -115,11 +115,22 @@ void dense_conv_prepare_weights(const DenseConvPlan& p, const float* w, int cin,
 void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, int hg, int* units,
                       int* nunits, unsigned long long* flop_px, int tau, int* list, int* lcount);
 long long* dense_conv_trace_buffer();
+unsigned long long* frame_trace_host();  // DFX_FRAME_TRACE: [64][4] frame-boundary stamps
 unsigned long long* trunc_trace_buffer();  // DFX_TRUNC_TRACE: [64 launches][1024 CTAs][8] globaltimer stamps  // microbenchmark stamps (DFX_CONV_DBG & 64)
 void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,
                        int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms);
 
 // ---- output (delta_layers.cpp:395-400) ----
-void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out);
+struct Readback {  // copied by the last kernel of a frame into mapped host memory
+    const uint8_t* src1;
+    int n1;
+    const uint8_t* src2;
+    int n2;
+    uint8_t* dst;  // device view of the page-locked host block
+};
+void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out, Readback rb);
+// First kernel of a frame: parameter block (mapped host -> device slot), counters zeroed, host ack.
+void launch_frame_begin(cudaStream_t s, const void* src, void* dst, size_t bytes, void* counters, size_t cnt_bytes,
+                        unsigned* ack, unsigned seq);
 
 }  // namespace dfx
