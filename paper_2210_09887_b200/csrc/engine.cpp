@@ -238,6 +238,12 @@ class Engine {
     unsigned* ack_d_ = nullptr;
     unsigned fseq_ = 0, pslot_seq_[2] = {0, 0};
     uint8_t* readback_d_ = nullptr;                // device view of readback_h_
+    // host path: copy-stream -> engine-stream flags [h2d slot 0, 1, d2h slot 0, 1]
+    DevArr<unsigned> hflags_;
+    const unsigned* pend_in_flag_ = nullptr;
+    unsigned pend_in_val_ = 0;
+    const unsigned* pend_out_flag_ = nullptr;
+    unsigned pend_out_val_ = 0;
     size_t params_bytes_ = 0, off_slots_ = 0, off_claims_ = 0, off_fresh_ = 0, off_own_ = 0;
     FrameDev* d_frame_ = nullptr;
     SlotDev* d_slots_ = nullptr;
@@ -684,7 +690,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     std::atomic_thread_fence(std::memory_order_release);
     launches_ = 0;
     launch_frame_begin(stream_, params_hd_[pslot_], params_d_.p + (size_t)pslot_ * pstride_, pstride_, counters_d_.p,
-                       cnt_bytes_, ack_d_, fseq_);
+                       cnt_bytes_, ack_d_, fseq_, pend_in_flag_, pend_in_val_);
     ++launches_;
     const Ctx C = ctx();
     cudaStream_t s = stream_;
@@ -799,7 +805,8 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
         }
     }
     const LayerRT& ort = lrt_[net_.out_layer];
-    const Readback rb{counters_d_.p, (int)(net_.layers.size() * 8 + 8), in_pkt_ext_.p, rows_ * cols_, readback_d_};
+    const Readback rb{counters_d_.p, (int)(net_.layers.size() * 8 + 8), in_pkt_ext_.p, rows_ * cols_, readback_d_,
+                      pend_out_flag_, pend_out_val_};
     PROF(DFX_FAM_DENSIFY, launch_densify(C, s, ort.acc, ort.aux, out_cur_ ? out_cur_ : out_d_.p, rb));
     CUDA_CHECK(cudaGetLastError());
 
@@ -1057,23 +1064,33 @@ void Engine::submit_host(const float* frame, int c, int h, int w, const float* h
         CUDA_CHECK(cudaDeviceSynchronize());
         hframe_d_[slot].alloc(fsz);
     }
+    if (!hflags_.p) {
+        hflags_.alloc(4);
+        CUDA_CHECK(cudaMemset(hflags_.p, 0, 4 * sizeof(unsigned)));
+    }
+    const unsigned v = (unsigned)(hseq_ + 1);
     // frame buffer free once the slot's previous frame finished computing
     CUDA_CHECK(cudaStreamWaitEvent(cstream_, ev_done_[slot], 0));
     CUDA_CHECK(cudaMemcpyAsync(hframe_d_[slot].p, frame, fsz * 4, cudaMemcpyHostToDevice, cstream_));
-    CUDA_CHECK(cudaEventRecord(ev_h2d_[slot], cstream_));
-    // output buffer free once the slot's previous output copy finished
-    CUDA_CHECK(cudaStreamWaitEvent(stream_, ev_h2d_[slot], 0));
-    CUDA_CHECK(cudaStreamWaitEvent(stream_, ev_d2h_[slot], 0));
+    launch_set_flag(cstream_, hflags_.p + slot, v);
+    // the engine stream takes no event dependency (that would cut its
+    // programmatic-launch chain): k_frame_begin polls the input flag, the
+    // output kernel polls the slot's previous copy-out flag
+    pend_in_flag_ = hflags_.p + slot;
+    pend_in_val_ = v;
+    pend_out_flag_ = hseq_ >= 2 ? hflags_.p + 2 + slot : nullptr;
+    pend_out_val_ = v - 2;
     if (initialized_ && hout_d_[slot].n < out_d_.n) hout_d_[slot].alloc(out_d_.n);
     out_cur_ = initialized_ ? hout_d_[slot].p : nullptr;
     enqueue(hframe_d_[slot].p, c, h, w, h9, nullptr);
+    pend_in_flag_ = pend_out_flag_ = nullptr;
     const float* result = out_cur_ ? out_cur_ : out_d_.p;
     out_cur_ = nullptr;
     CUDA_CHECK(cudaEventRecord(ev_done_[slot], stream_));
     const size_t n = (size_t)pending_.out_channels * pending_.out_height * pending_.out_width;
     CUDA_CHECK(cudaStreamWaitEvent(dstream_, ev_done_[slot], 0));
     if (out && cap >= n) CUDA_CHECK(cudaMemcpyAsync(out, result, n * 4, cudaMemcpyDeviceToHost, dstream_));
-    CUDA_CHECK(cudaEventRecord(ev_d2h_[slot], dstream_));
+    launch_set_flag(dstream_, hflags_.p + 2 + slot, v);
     ++hseq_;
 }
 

@@ -375,10 +375,32 @@ __global__ void k_input_apply(Ctx c, const float* __restrict__ aligned, const ui
 // frame: the copy runs BEFORE the dependency wait, overlapping the previous
 // frame's last kernel, which reads the other slot.
 __device__ unsigned g_begin_done;
+// Cross-stream handshake without stream events (which would cut the engine
+// stream's programmatic-launch chain): a copy stream publishes "copy n done"
+// with k_set_flag, the engine kernel that depends on it polls (bounded: traps
+// after ~4 s instead of hanging the GPU).
+__global__ void k_set_flag(unsigned* f, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_flag(const unsigned* f, unsigned v) {
+    if (!f) return;
+    if (threadIdx.x == 0) {
+        unsigned x;
+        for (long long it = 0;; ++it) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(f) : "memory");
+            if ((int)(x - v) >= 0) break;
+            if (it > (1LL << 24)) __trap();
+            __nanosleep(256);
+        }
+    }
+    __syncthreads();
+}
 __global__ void k_frame_begin(const uint4* __restrict__ src, uint4* __restrict__ dst, int n16,
-                              uint4* __restrict__ counters, int cnt16, volatile unsigned* ack, unsigned seq) {
+                              uint4* __restrict__ counters, int cnt16, volatile unsigned* ack, unsigned seq,
+                              const unsigned* in_flag, unsigned in_val) {
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     for (int i = tid; i < n16; i += nth) dst[i] = src[i];
+    wait_flag(in_flag, in_val);  // host path: this frame's input copy has landed
     pdl_enter();
     for (int i = tid; i < cnt16; i += nth) counters[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
@@ -1146,6 +1168,7 @@ __device__ __forceinline__ void frame_readback(const Readback& rb) {
 }
 __global__ void k_densify8(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ out, int trace, Readback rb) {
     pdl_enter();
+    wait_flag(rb.out_flag, rb.out_val);  // host path: the output slot's previous copy-out is done
     frame_readback(rb);
     const FrameDev& F = *c.f;
     const int t = acc.t, C = acc.C, G = C / 8;
@@ -1186,6 +1209,7 @@ __global__ void k_densify8(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ 
 
 __global__ void k_densify(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ out, Readback rb) {
     pdl_enter();
+    wait_flag(rb.out_flag, rb.out_val);
     frame_readback(rb);
     const FrameDev& F = *c.f;
     const int t = acc.t, C = acc.C;
@@ -1360,10 +1384,11 @@ void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, floa
                out, rb);
 }
 void launch_frame_begin(cudaStream_t s, const void* src, void* dst, size_t bytes, void* counters, size_t cnt_bytes,
-                        unsigned* ack, unsigned seq) {
+                        unsigned* ack, unsigned seq, const unsigned* in_flag, unsigned in_val) {
     launch_pdl(k_frame_begin, 32, kThreads, 0, s, reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst),
                (int)(bytes / 16), reinterpret_cast<uint4*>(counters), (int)(cnt_bytes / 16), (volatile unsigned*)ack,
-               seq);
+               seq, in_flag, in_val);
 }
+void launch_set_flag(cudaStream_t s, unsigned* f, unsigned v) { k_set_flag<<<1, 1, 0, s>>>(f, v); }
 
 }  // namespace dfx

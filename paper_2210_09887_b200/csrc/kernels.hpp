@@ -127,10 +127,14 @@ struct Readback {  // copied by the last kernel of a frame into mapped host memo
     const uint8_t* src2;
     int n2;
     uint8_t* dst;  // device view of the page-locked host block
+    const unsigned* out_flag = nullptr;  // host path: wait until *out_flag >= out_val before writing the output
+    unsigned out_val = 0;
 };
 void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out, Readback rb);
 // First kernel of a frame: parameter block (mapped host -> device slot), counters zeroed, host ack.
 void launch_frame_begin(cudaStream_t s, const void* src, void* dst, size_t bytes, void* counters, size_t cnt_bytes,
-                        unsigned* ack, unsigned seq);
+                        unsigned* ack, unsigned seq, const unsigned* in_flag = nullptr, unsigned in_val = 0);
+// copy-stream -> engine-stream handshake: *f = v (release) once the stream's prior work is done
+void launch_set_flag(cudaStream_t s, unsigned* f, unsigned v);
 
 }  // namespace dfx
