@@ -416,23 +416,30 @@ __device__ __forceinline__ void store_cols(uint32_t taddr, const uint32_t* v) {
 
 template <int KC>
 __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArgs a) {
-    pdl_enter();
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar_full[8], bar_empty[8], bar_pf[kMaxPB], bar_pe[kMaxPB], bar_af[2], bar_ae[2];
     __shared__ uint32_t tmem_base_sh;
     __shared__ int s_last;
     __shared__ int s_poff[2 * 22 * 14];  // per-pixel patch source offsets (k <= 7, two units)
 
-    const FrameDev& F = *c.f;
-    const int listed = *a.nunits;
-    const int n = dense_units(a, listed);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int K2 = a.k * a.k;
     const int nKB = a.nCB * K2;
-    const DenseSched sch = dense_sched(n, a.nNB, nKB, a.smax, a.sms, a.umax);
-    const int S = sch.S, UPI = sch.U, items = sch.items;
-    if ((int)blockIdx.x >= items) return;
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // Before the dependency wait (nothing here reads the previous kernel's
+    // output): start the layer's weights towards L2 (one bulk prefetch per CTA
+    // over its slice), allocate TMEM and initialise the barriers, so the wait
+    // is followed directly by the first patch.
+    if (tid == 0) {
+        const size_t wbytes = (size_t)a.nNB * nKB * a.w_stage;
+        const size_t per = ((wbytes + gridDim.x - 1) / gridDim.x + 255) / 256 * 256;
+        const size_t o0 = per * blockIdx.x;
+        if (o0 < wbytes) {
+            const uint32_t sz = (uint32_t)(o0 + per <= wbytes ? per : wbytes - o0);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const uint8_t*>(a.w) + o0),
+                         "r"(sz)
+                         : "memory");
+        }
+    }
     const int PW = a.tpu ? (1 << a.tsh) + 2 * a.r : kUX + 2 * a.r;  // patch row pitch (pixels)
     const int NST = a.nst;
     // TMEM: accumulators [nbuf][2 units][NBD] then NST A stages of [2 units][hi KC | lo KC]
@@ -461,6 +468,16 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_enter();
+    const FrameDev& F = *c.f;
+    const int listed = *a.nunits;
+    const int n = dense_units(a, listed);
+    const DenseSched sch = dense_sched(n, a.nNB, nKB, a.smax, a.sms, a.umax);
+    const int S = sch.S, UPI = sch.U, items = sch.items;
+    if ((int)blockIdx.x >= items) {  // no work this frame: give the TMEM back
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh), "r"(512));
+        return;
+    }
     const uint32_t tmem = tmem_base_sh;
     const uint32_t sbase = smem_u32(smem);
     if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) a.trace[500] = clock64();
