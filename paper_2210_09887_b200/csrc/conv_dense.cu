@@ -1089,4 +1089,6 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
     // split-K partials are reduced inside k_conv_dense (last-arriving CTA)
 }
 
+DFX_KTRACE_SETTER(ktrace_set_dense)
+
 }  // namespace dfx

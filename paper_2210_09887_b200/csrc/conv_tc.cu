@@ -548,4 +548,6 @@ void launch_conv_tc(const Ctx& c, cudaStream_t s, PktDev in, const float* wsplit
     }
 }
 
+DFX_KTRACE_SETTER(ktrace_set_tc)
+
 }  // namespace dfx

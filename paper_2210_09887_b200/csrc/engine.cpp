@@ -1409,6 +1409,31 @@ int dfx_debug_conv_trace(long long* out, int n) {
                    "trace copy failed");
     });
 }
+// Debug: chain trace (DFX_KTRACE): enable with a device buffer of 4096 stamps
+// + counter (on = 1), or copy the stamps and the count out (on = 0).
+int dfx_debug_ktrace(int on, unsigned long long* out, unsigned* count) {
+    return guard([&] {
+        static unsigned long long* buf = nullptr;
+        static unsigned* ctr = nullptr;
+        if (on) {
+            if (!buf) {
+                dfx::check(cudaMalloc(&buf, 4096 * 8) == cudaSuccess && cudaMalloc(&ctr, 4) == cudaSuccess, "ktrace alloc");
+            }
+            cudaMemset(buf, 0, 4096 * 8);
+            cudaMemset(ctr, 0, 4);
+            dfx::ktrace_set_kernels(buf, ctr);
+            dfx::ktrace_set_hbm(buf, ctr);
+            dfx::ktrace_set_dense(buf, ctr);
+            dfx::ktrace_set_tc(buf, ctr);
+            cudaDeviceSynchronize();
+        } else {
+            dfx::check(buf != nullptr, "ktrace not enabled");
+            cudaDeviceSynchronize();
+            cudaMemcpy(out, buf, 4096 * 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(count, ctr, 4, cudaMemcpyDeviceToHost);
+        }
+    });
+}
 // Debug: frame-boundary stamps (DFX_FRAME_TRACE=1), [64][4] u64.
 int dfx_debug_frame_trace(unsigned long long* out) {
     return guard([&] { memcpy(out, dfx::frame_trace_host(), 64 * 4 * 8); });

@@ -1391,4 +1391,6 @@ void launch_frame_begin(cudaStream_t s, const void* src, void* dst, size_t bytes
 }
 void launch_set_flag(cudaStream_t s, unsigned* f, unsigned v) { k_set_flag<<<1, 1, 0, s>>>(f, v); }
 
+DFX_KTRACE_SETTER(ktrace_set_kernels)
+
 }  // namespace dfx

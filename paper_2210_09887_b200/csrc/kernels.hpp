@@ -115,6 +115,11 @@ void dense_conv_prepare_weights(const DenseConvPlan& p, const float* w, int cin,
 void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, int hg, int* units,
                       int* nunits, unsigned long long* flop_px, int tau, int* list, int* lcount);
 long long* dense_conv_trace_buffer();
+// DFX_KTRACE chain trace: per-translation-unit setters of the stamp buffer
+void ktrace_set_kernels(unsigned long long* b, unsigned* c);
+void ktrace_set_hbm(unsigned long long* b, unsigned* c);
+void ktrace_set_dense(unsigned long long* b, unsigned* c);
+void ktrace_set_tc(unsigned long long* b, unsigned* c);
 unsigned long long* frame_trace_host();  // DFX_FRAME_TRACE: [64][4] frame-boundary stamps
 unsigned long long* trunc_trace_buffer();  // DFX_TRUNC_TRACE: [64 launches][1024 CTAs][8] globaltimer stamps  // microbenchmark stamps (DFX_CONV_DBG & 64)
 void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,

@@ -540,4 +540,6 @@ bool launch_maxpool_vec(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, Buf
     return true;
 }
 
+DFX_KTRACE_SETTER(ktrace_set_hbm)
+
 }  // namespace dfx

@@ -16,10 +16,32 @@
 
 namespace dfx {
 
+// Chain trace (DFX_KTRACE=1, development only): CTA 0 of every kernel stamps
+// %globaltimer when its dependency wait returns, i.e. when the previous kernel
+// of the stream has completed; consecutive stamps are the per-kernel time in
+// the real (overlapped) launch chain. TU-local pointers, set per translation
+// unit by its DFX_KTRACE_SETTER.
+namespace {
+__device__ unsigned long long* g_kt_buf;
+__device__ unsigned* g_kt_ctr;
+}  // namespace
 __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long* b = g_kt_buf;
+        if (b) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            b[atomicAdd(g_kt_ctr, 1u) & 4095u] = t;
+        }
+    }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+#define DFX_KTRACE_SETTER(name)                                     \
+    void name(unsigned long long* b, unsigned* c) {                 \
+        cudaMemcpyToSymbol(g_kt_buf, &b, sizeof b);                 \
+        cudaMemcpyToSymbol(g_kt_ctr, &c, sizeof c);                 \
+    }
 
 inline bool pdl_enabled() {
     static const int on = [] {
