@@ -420,6 +420,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     __shared__ __align__(8) uint64_t bar_full[8], bar_empty[8], bar_pf[kMaxPB], bar_pe[kMaxPB], bar_af[2], bar_ae[2];
     __shared__ uint32_t tmem_base_sh;
     __shared__ int s_last;
+    __shared__ int s_red_it;  // item whose split-K partials this CTA reduces at the end (-1: none)
     __shared__ int s_poff[2 * 22 * 14];  // per-pixel patch source offsets (k <= 7, two units)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -450,6 +451,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                      "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    if (tid == 0) s_red_it = -1;
     if (tid == 32) {
         for (int i = 0; i < NST; ++i) {
             mbar_init(smem_u32(&bar_full[i]), 5);  // 4 A-producer warps + the weight bytes
@@ -481,6 +483,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     const uint32_t tmem = tmem_base_sh;
     const uint32_t sbase = smem_u32(smem);
     if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) a.trace[500] = clock64();
+    if ((a.dbg & 64) && tid == 0 && blockIdx.x < 400) {  // per-CTA start (after the wait), %globaltimer
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[1100 + 2 * blockIdx.x] = (long long)t;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        if (blockIdx.x < 148) a.trace[1900 + blockIdx.x] = smid;
+    }
     // smem: patches [2 buffers][2 units][hi, lo] planes, then the weight stages
     const uint32_t unit_bytes = a.patch_bytes, buf_bytes = a.umax * unit_bytes;
     const uint32_t w_base = sbase + a.npb * buf_bytes;
@@ -702,47 +712,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                     s_last = atomicAdd(a.cnt + it / S, 1) == S - 1;
                 }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (s_last) {
-                    __threadfence();
-                    for (int j = 0; j < nu; ++j) {
-                        const int u = UPI * pr + j;
-                        int y, x;
-                        if (!unit_pixel(a, listed, u, m, y, x)) continue;
-                        if (!(y >= -hs && y < eh && x >= -hs && x < ew)) continue;
-                        float* dst = a.out.d + pkt_off(a.out, y, x);
-                        const int o1 = min(a.cout, (nb + 1) * a.NBD);
-                        const size_t sstride = (size_t)n * 128 * a.cout_pad;
-                        // 8 float4 per split in flight per step (the partials sit in L2)
-                        for (int ob = nb * a.NBD; ob < o1; ob += 32) {
-                            const float* src = a.ws + ((size_t)u * 128 + m) * a.cout_pad + ob;
-                            float4 acc4[8];
-#pragma unroll
-                            for (int q4 = 0; q4 < 8; ++q4) acc4[q4] = __ldcg(reinterpret_cast<const float4*>(src) + q4);
-                            for (int sp = 1; sp < S; ++sp) {
-                                float4 v[8];
-#pragma unroll
-                                for (int q4 = 0; q4 < 8; ++q4)
-                                    v[q4] = __ldcg(reinterpret_cast<const float4*>(src + sp * sstride) + q4);
-#pragma unroll
-                                for (int q4 = 0; q4 < 8; ++q4) {
-                                    acc4[q4].x = __fadd_rn(acc4[q4].x, v[q4].x), acc4[q4].y = __fadd_rn(acc4[q4].y, v[q4].y);
-                                    acc4[q4].z = __fadd_rn(acc4[q4].z, v[q4].z), acc4[q4].w = __fadd_rn(acc4[q4].w, v[q4].w);
-                                }
-                            }
-#pragma unroll
-                            for (int q4 = 0; q4 < 8; ++q4) {
-                                const int o = ob + 4 * q4;
-                                if ((a.out.C & 3) == 0 && o + 4 <= o1) {
-                                    *reinterpret_cast<float4*>(dst + o) = acc4[q4];
-                                } else {
-                                    const float vv[4] = {acc4[q4].x, acc4[q4].y, acc4[q4].z, acc4[q4].w};
-                                    for (int e = 0; e < 4 && o + e < o1; ++e) dst[o + e] = vv[e];
-                                }
-                            }
-                        }
-                    }
-                    if (q == 0 && lane == 0) a.cnt[it / S] = 0;
-                }
+                // the last-arriving CTA reduces at the end of the kernel with ALL its
+                // threads (S > 1 implies one item per CTA): 128 epilogue threads alone
+                // made it a chain of dependent L2 round trips at the layer's tail
+                if (s_last && q == 0 && lane == 0) s_red_it = it;
             }
             if ((a.dbg & 64) && blockIdx.x == 0 && tid == 128 * kProdWG + 128 && ui < 4) {
                 a.trace[504 + 2 * ui] = t_e0;
@@ -857,7 +830,57 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (s_red_it >= 0) {
+        // fixed-order (split 0, 1, ...) sum of the S partials of one (unit group,
+        // N-block) tile into the packet: every thread takes float4 columns of rows,
+        // all S loads of a float4 in flight before the adds (deterministic order)
+        __threadfence();
+        const int it = s_red_it;
+        int pr, nb, kb0, kb1;
+        item_info(it, pr, nb, kb0, kb1);
+        const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
+        const int hs = a.out.halo;
+        const int eh = F.th * a.out.t + hs, ew = F.tw * a.out.t + hs;
+        const int o0 = nb * a.NBD, o1 = min(a.cout, (nb + 1) * a.NBD);
+        const int nq = (o1 - o0 + 3) / 4;  // float4 columns per row
+        const size_t sstride = (size_t)n * 128 * a.cout_pad;
+        const bool vec = (a.out.C & 3) == 0;
+        for (int e = tid; e < nu * 128 * nq; e += blockDim.x) {
+            const int j = e / (128 * nq), rem = e - j * 128 * nq;
+            const int m = rem / nq, c4 = rem - m * nq;
+            const int u = UPI * pr + j;
+            int y, x;
+            if (!unit_pixel(a, listed, u, m, y, x)) continue;
+            if (!(y >= -hs && y < eh && x >= -hs && x < ew)) continue;
+            const int o = o0 + 4 * c4;
+            const float* src = a.ws + ((size_t)u * 128 + m) * a.cout_pad + o;
+            float4 v[8];
+#pragma unroll
+            for (int sp = 0; sp < 8; ++sp)
+                if (sp < S) v[sp] = __ldcg(reinterpret_cast<const float4*>(src + sp * sstride));
+            float4 acc4 = v[0];
+#pragma unroll
+            for (int sp = 1; sp < 8; ++sp)
+                if (sp < S) {
+                    acc4.x = __fadd_rn(acc4.x, v[sp].x), acc4.y = __fadd_rn(acc4.y, v[sp].y);
+                    acc4.z = __fadd_rn(acc4.z, v[sp].z), acc4.w = __fadd_rn(acc4.w, v[sp].w);
+                }
+            float* dst = a.out.d + pkt_off(a.out, y, x) + o;
+            if (vec && o + 4 <= o1) {
+                *reinterpret_cast<float4*>(dst) = acc4;
+            } else {
+                const float vv[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
+                for (int q = 0; q < 4 && o + q < o1; ++q) dst[q] = vv[q];
+            }
+        }
+        if (tid == 0) a.cnt[it / S] = 0;
+    }
     if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) a.trace[501] = clock64();
+    if ((a.dbg & 64) && tid == 0 && blockIdx.x < 400) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[1101 + 2 * blockIdx.x] = (long long)t;
+    }
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
@@ -1068,7 +1091,7 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
                 p.KC, p.nCB, p.NBD, p.nNB, p.nstw, p.smax > 1 ? p.smax : 1, num_sms, p.s_c4, p.patch_bytes,
                 p.w_stage, p.acc_cols, p.nbuf, p.nbuf * p.acc_cols, p.umax, p.tpu, p.tsh, p.patch_px, p.npb,
                 p.nmma, nullptr, 0};
-    if (getenv("DFX_CONV_DBG") && !g_trace) cudaMalloc(&g_trace, 1024 * 8);
+    if (getenv("DFX_CONV_DBG") && !g_trace) cudaMalloc(&g_trace, 2048 * 8);
     a.trace = g_trace;
     if (const char* d = getenv("DFX_CONV_DBG")) a.dbg = atoi(d);
     if (const char* d = getenv("DFX_CONV_TRACE_IDX")) {  // trace only the i-th dense launch of every 8

@@ -13,8 +13,8 @@ e = dfx.DeltaEngine(spec, dfx.EngineConfig(**cfg, conv_mode="tf32x3"))
 for f, H in seq:
     e.run_frame_full(f, H)
 lib, _ = _capi.load_library()
-tr = np.zeros(1024, dtype=np.int64)
-assert lib.dfx_debug_conv_trace(tr.ctypes.data_as(C.POINTER(C.c_longlong)), 1024) == 0
+tr = np.zeros(2048, dtype=np.int64)
+assert lib.dfx_debug_conv_trace(tr.ctypes.data_as(C.POINTER(C.c_longlong)), 2048) == 0
 b = tr[500]
 print(f"kernel (CTA 0) {tr[501] - b} cycles; epilogue items:",
       [(int(tr[504 + 2 * i] - b), int(tr[505 + 2 * i] - b)) for i in range(4)])
@@ -38,3 +38,20 @@ if len(seg):
     print("producer K-block segments (median / max cycles):", ", ".join(f"{n} {np.median(seg[:, b] - seg[:, a]):.0f}/{(seg[:, b] - seg[:, a]).max()}" for n, a, b in names))
     wg0 = seg[0::3]
     print("WG0 arrive -> next start gaps:", [int(wg0[i + 1, 0] - wg0[i, 2]) for i in range(min(12, len(wg0) - 1))])
+cta = tr[1100:1900].reshape(400, 2)
+cta = cta[(cta[:, 0] > 0) & (np.abs(cta[:, 0] - tr[1100]) < 200000)]  # this launch only (stale slots from earlier launches)
+if len(cta):
+    t0 = cta[:, 0].min()
+    st, en = (cta[:, 0] - t0) / 1e3, (cta[:, 1] - t0) / 1e3
+    print(f"CTAs {len(cta)}: start spread {st.max():.1f} us; end min/median/max {en.min():.1f}/{np.median(en):.1f}/{en.max():.1f} us")
+    print("slowest CTAs:", [(int(i), round(float(en[i]), 1)) for i in np.argsort(-en)[:8]])
+full = tr[1100:1900].reshape(400, 2)
+ok = (full[:, 0] > 0) & (np.abs(full[:, 0] - tr[1100]) < 200000)
+idx = np.nonzero(ok[:148])[0]
+if len(idx):
+    t0 = full[idx, 0].min()
+    en = (full[idx, 1] - t0) / 1e3
+    sm = tr[1900 + idx]
+    order = np.argsort(-en)
+    print("slowest (cta, smid, end us):", [(int(idx[i]), int(sm[i]), round(float(en[i]), 1)) for i in order[:12]])
+    print("fastest (cta, smid, end us):", [(int(idx[i]), int(sm[i]), round(float(en[i]), 1)) for i in order[-6:]])
