@@ -712,10 +712,12 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                     s_last = atomicAdd(a.cnt + it / S, 1) == S - 1;
                 }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
-                // the last-arriving CTA reduces at the end of the kernel with ALL its
-                // threads (S > 1 implies one item per CTA): 128 epilogue threads alone
-                // made it a chain of dependent L2 round trips at the layer's tail
-                if (s_last && q == 0 && lane == 0) s_red_it = it;
+                // every split CTA reduces 1/S of the tile's rows at the end of the
+                // kernel with ALL its threads once the S partials are in (S > 1
+                // implies one item per CTA, all CTAs resident: the wait cannot
+                // deadlock); 128 epilogue threads of one CTA made it a chain of
+                // dependent L2 round trips at the layer's tail
+                if (q == 0 && lane == 0) s_red_it = it;
             }
             if ((a.dbg & 64) && blockIdx.x == 0 && tid == 128 * kProdWG + 128 && ui < 4) {
                 a.trace[504 + 2 * ui] = t_e0;
@@ -832,10 +834,22 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     tc_fence_after();
     if (s_red_it >= 0) {
         // fixed-order (split 0, 1, ...) sum of the S partials of one (unit group,
-        // N-block) tile into the packet: every thread takes float4 columns of rows,
-        // all S loads of a float4 in flight before the adds (deterministic order)
-        __threadfence();
+        // N-block) tile into the packet: this split CTA takes rows [ks*128/S,
+        // (ks+1)*128/S), every thread float4 columns of those rows, all S loads of
+        // a float4 in flight before the adds (deterministic order)
         const int it = s_red_it;
+        if (tid == 0) {
+            unsigned v;
+            for (long long spin = 0;; ++spin) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.cnt + it / S) : "memory");
+                if ((int)v >= S) break;
+                if (spin > (1LL << 26)) __trap();
+                __nanosleep(64);
+            }
+        }
+        __syncthreads();
+        __threadfence();
+        const int ks = it % S, m0 = 128 * ks / S, m1 = 128 * (ks + 1) / S, nm = m1 - m0;
         int pr, nb, kb0, kb1;
         item_info(it, pr, nb, kb0, kb1);
         const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
@@ -845,9 +859,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
         const int nq = (o1 - o0 + 3) / 4;  // float4 columns per row
         const size_t sstride = (size_t)n * 128 * a.cout_pad;
         const bool vec = (a.out.C & 3) == 0;
-        for (int e = tid; e < nu * 128 * nq; e += blockDim.x) {
-            const int j = e / (128 * nq), rem = e - j * 128 * nq;
-            const int m = rem / nq, c4 = rem - m * nq;
+        for (int e = tid; e < nu * nm * nq; e += blockDim.x) {
+            const int j = e / (nm * nq), rem = e - j * nm * nq;
+            const int m = m0 + rem / nq, c4 = rem - (rem / nq) * nq;
             const int u = UPI * pr + j;
             int y, x;
             if (!unit_pixel(a, listed, u, m, y, x)) continue;
@@ -873,7 +887,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                 for (int q = 0; q < 4 && o + q < o1; ++q) dst[q] = vv[q];
             }
         }
-        if (tid == 0) a.cnt[it / S] = 0;
+        __syncthreads();
+        if (tid == 0) {  // second round of arrivals: the last reducer re-arms the counter
+            if (atomicAdd(a.cnt + it / S, 1) == 2 * S - 1) a.cnt[it / S] = 0;
+        }
     }
     if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) a.trace[501] = clock64();
     if ((a.dbg & 64) && tid == 0 && blockIdx.x < 400) {
