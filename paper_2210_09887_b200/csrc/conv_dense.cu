@@ -171,21 +171,43 @@ __device__ __forceinline__ bool is_target_s1(const PktDev& in, int th, int tw, i
 // (uy + 1) << 16 | (ux + 1)), and zeros for the pixels of active stored tiles
 // that no dense unit covers (possible only when a tile holds several units).
 constexpr int kPlanThreads = 256;
-__global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, PktDev out, int k, int r, int hg,
-                                                            int nbw, int* __restrict__ units,
-                                                            int* __restrict__ nunits,
-                                                            unsigned long long* __restrict__ flop_px, int tau,
-                                                            int* __restrict__ list, int* __restrict__ lcount,
-                                                            int tile_units) {
-    pdl_enter();
-    __shared__ uint32_t s_bits[4096 / 32];
-    __shared__ int s_ucnt[32];
-    __shared__ int s_tstore[32];
-    __shared__ int s_geo[kPlanThreads / 32];
+struct PlanArgs {
+    PktDev in, out;
+    int k, r, hg, nbw, nblocks;
+    int* units;
+    int* nunits;
+    unsigned long long* flop_px;
+    int tau;
+    int* list;
+    int* lcount;
+    int tile_units;
+};
+struct PlanSmem {
+    uint32_t bits[4096 / 32];
+    int ucnt[32];
+    int tstore[32];
+    int geo[32];
+};
+// One plan block, executed by the NT threads of the calling CTA (the
+// k_conv_plan CTA; NT = threads taking part).
+template <int NT>
+__device__ void plan_block(const Ctx& c, const PlanArgs& pa, int blk, PlanSmem& sm) {
+    const PktDev& in = pa.in;
+    const PktDev& out = pa.out;
+    const int k = pa.k, r = pa.r, hg = pa.hg, nbw = pa.nbw, tau = pa.tau, tile_units = pa.tile_units;
+    int* __restrict__ units = pa.units;
+    int* __restrict__ nunits = pa.nunits;
+    unsigned long long* __restrict__ flop_px = pa.flop_px;
+    int* __restrict__ list = pa.list;
+    int* __restrict__ lcount = pa.lcount;
+    uint32_t* s_bits = sm.bits;
+    int* s_ucnt = sm.ucnt;
+    int* s_tstore = sm.tstore;
+    int* s_geo = sm.geo;
     const FrameDev& F = *c.f;
     const int t = out.t;
     const int BH = t > kUY ? t : kUY, BW = t > kUX ? t : kUX;
-    const int by = blockIdx.x / nbw, bx = blockIdx.x - (blockIdx.x / nbw) * nbw;
+    const int by = blk / nbw, bx = blk - (blk / nbw) * nbw;
     const int Y0 = (by - 1) * BH, X0 = (bx - 1) * BW;
     const int eh = F.th * t, ew = F.tw * t;
     const int hs = out.halo;
@@ -201,7 +223,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
     __syncthreads();
     const int npx = BH * BW;
     int geo = 0;
-    for (int p0 = 0; p0 < npx; p0 += kPlanThreads) {
+    for (int p0 = 0; p0 < npx; p0 += NT) {
         const int p = p0 + threadIdx.x;
         bool tgt = false;
         int uid = -1;
@@ -226,7 +248,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
     __syncthreads();
     if (threadIdx.x == 0) {
         int tot = 0;
-        for (int w = 0; w < kPlanThreads / 32; ++w) tot += s_geo[w];
+        for (int w = 0; w < NT / 32; ++w) tot += s_geo[w];
         if (tot) atomicAdd(flop_px, (unsigned long long)tot);  // one global atomic per block
     }
     // units with >= tau targets are computed whole by k_conv_dense (tile-unit
@@ -237,7 +259,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
     }
     // targets of sparser units go to the gathered kernel (stored extent only)
     if (tau > 1) {
-        for (int p0 = 0; p0 < npx; p0 += kPlanThreads) {
+        for (int p0 = 0; p0 < npx; p0 += NT) {
             const int p = p0 + threadIdx.x;
             bool g = false;
             int y = 0, x = 0;
@@ -267,7 +289,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
         const int C = out.C;
         const int per = (C & 3) == 0 ? C / 4 : C;
         const FDiv dper(per);
-        for (int e = threadIdx.x; e < npx * per; e += kPlanThreads) {
+        for (int e = threadIdx.x; e < npx * per; e += NT) {
             const int p = dper(e), q = e - p * per;
             const int ly = dbw(p), lx = p - ly * BW;
             if (s_ucnt[(ly / kUY) * upr + lx / kUX] >= tau || !s_tstore[dt(ly) * tpr + dt(lx)] ||
@@ -281,6 +303,12 @@ __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PktDev in, Pk
                 out.d[pkt_off(out, y, x) + q] = 0.0f;
         }
     }
+}
+
+__global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PlanArgs pa) {
+    pdl_enter();
+    __shared__ PlanSmem sm;
+    plan_block<kPlanThreads>(c, pa, blockIdx.x, sm);
 }
 
 struct DenseArgs {
@@ -320,14 +348,14 @@ __device__ __forceinline__ int dense_units(const DenseArgs& a, int listed) {
 // Output pixel of row m of unit u (false: padding row of a partial tile unit).
 __device__ __forceinline__ bool unit_pixel(const DenseArgs& a, int listed, int u, int m, int& y, int& x) {
     if (a.tpu == 0) {
-        const int uv = __ldg(a.units + u);
+        const int uv = __ldcg(a.units + u);
         y = ((uv >> 16) - 1) * kUY + (m >> 3), x = ((uv & 0xffff) - 1) * kUX + (m & 7);
         return true;
     }
     const int s = m >> (2 * a.tsh), l = m & ((1 << (2 * a.tsh)) - 1);
     const int li = u * a.tpu + s;
     if (li >= listed) return false;
-    const int tv = __ldg(a.units + li);
+    const int tv = __ldcg(a.units + li);
     y = (((tv >> 16) - 8) << a.tsh) + (l >> a.tsh);
     x = (((tv & 0xffff) - 8) << a.tsh) + (l & ((1 << a.tsh) - 1));
     return true;
@@ -472,7 +500,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     tc_fence_after();
     pdl_enter();
     const FrameDev& F = *c.f;
-    const int listed = *a.nunits;
+    const int listed = __ldcg(a.nunits);
     const int n = dense_units(a, listed);
     const DenseSched sch = dense_sched(n, a.nNB, nKB, a.smax, a.sms, a.umax);
     const int S = sch.S, UPI = sch.U, items = sch.items;
@@ -587,7 +615,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
             if (!a.tpu) {
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
-                    const int uv = __ldg(a.units + UPI * pr + (j < nu ? j : 0));
+                    const int uv = __ldcg(a.units + UPI * pr + (j < nu ? j : 0));
                     y0[j] = ((uv >> 16) - 1) * kUY - a.r;
                     x0[j] = ((uv & 0xffff) - 1) * kUX - a.r;
                 }
@@ -605,7 +633,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                     const int py = l / PW, px = l - py * PW;
                     const int li = pr * a.tpu + s;
                     ok = li < listed;
-                    const int tv = ok ? __ldg(a.units + li) : 0;
+                    const int tv = ok ? __ldcg(a.units + li) : 0;
                     y = (((tv >> 16) - 8) << a.tsh) - a.r + py;
                     x = (((tv & 0xffff) - 8) << a.tsh) - a.r + px;
                 } else {
@@ -986,7 +1014,7 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     size_t budget = kDenseSmemBudget;
     if (const char* e = getenv("DFX_DENSE_SMEM_KB")) {  // experiments: smaller shared-memory plans
         const size_t v = (size_t)atoi(e) * 1024;
-        if (v >= 64 * 1024 && v <= 224 * 1024) budget = v;
+        if (v >= 64 * 1024 && v <= 220 * 1024) budget = v;
     }
     auto set_kc = [&](int kc) {
         p.KC = kc;
@@ -1085,15 +1113,15 @@ void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktD
                       int* nunits, unsigned long long* flop_px, int tau, int* list, int* lcount) {
     if (hg > 8) throw std::runtime_error("conv_plan: grown halo > 8 px");
     if (p.tpu && out.RT >= 8) throw std::runtime_error("conv_plan: tile ring too wide for tile units");
-    launch_pdl(k_conv_plan, p.nbh * p.nbw, kPlanThreads, 0, s, c, in, out, p.k, p.r, hg, p.nbw, units, nunits, flop_px,
-               tau, list, lcount, p.tpu ? 1 : 0);
+    const PlanArgs pa{in, out, p.k, p.r, hg, p.nbw, p.nbh * p.nbw, units, nunits, flop_px, tau, list, lcount, p.tpu ? 1 : 0};
+    launch_pdl(k_conv_plan, p.nbh * p.nbw, kPlanThreads, 0, s, c, pa);
 }
 
 template <int KC>
 static void launch_kc(int grid, size_t smem, cudaStream_t s, const Ctx& c, const DenseArgs& a) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_conv_dense<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
+        cudaFuncSetAttribute(k_conv_dense<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         configured = true;
     }
     launch_pdl(k_conv_dense<KC>, grid, kDenseThreads, smem, s, c, a);

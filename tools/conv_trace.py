@@ -55,3 +55,4 @@ if len(idx):
     order = np.argsort(-en)
     print("slowest (cta, smid, end us):", [(int(idx[i]), int(sm[i]), round(float(en[i]), 1)) for i in order[:12]])
     print("fastest (cta, smid, end us):", [(int(idx[i]), int(sm[i]), round(float(en[i]), 1)) for i in order[-6:]])
+print("loader startup (cycles from kernel start): poff begin %d, poff done %d, bar %d, cp.async issued %d, landed %d, pe ok %d" % tuple(int(tr[560 + i] - b) for i in range(6)))
