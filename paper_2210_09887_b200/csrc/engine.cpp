@@ -707,8 +707,16 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
 
     // input stage
     if (!integer) PROF(DFX_FAM_INPUT, launch_warp(C, s, frame_dev, c, warped_d_.p, fp_d_.p));
-    PROF(DFX_FAM_INPUT, launch_align(C, s, frame_dev, warped_d_.p, fp_d_.p, c, aligned_d_.p, valid_d_.p, canvas_pitch_, T));
     if (cropped && !integer) PROF(DFX_FAM_INPUT, launch_count_dropped(C, s, fp_d_.p, T, dropped));
+    static const bool fuse_input = !(getenv("DFX_FUSE_INPUT") && getenv("DFX_FUSE_INPUT")[0] == '0');
+    if (fuse_input && !F.roi && !cfg_.noise_suppression) {
+        // two launches: align + coverage + significance, then gate + input truncation
+        PROF(DFX_FAM_INPUT, launch_input_tile_a(C, s, frame_dev, warped_d_.p, fp_d_.p, c, aligned_d_.p, canvas_pitch_, T,
+                                                in_acc_, in_trunc_, cfg_.input_threshold, cov_d_.p, sig_d_.p));
+        PROF(DFX_FAM_INPUT, launch_input_tile_b(C, s, aligned_d_.p, cov_d_.p, sig_d_.p, d_fresh_, cfg_.mask_dilation,
+                                                canvas_pitch_, in_acc_, in_trunc_, in_pkt_));
+    } else {
+    PROF(DFX_FAM_INPUT, launch_align(C, s, frame_dev, warped_d_.p, fp_d_.p, c, aligned_d_.p, valid_d_.p, canvas_pitch_, T));
     const float* fac = nullptr;
     if (F.roi) {
         if (!integer) PROF(DFX_FAM_INPUT, launch_warp(C, s, roi_dev, 1, roi_warped_d_.p, roi_fp_d_.p));
@@ -727,6 +735,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     }
     PROF(DFX_FAM_INPUT, launch_gate(C, s, sig, cov_d_.p, d_fresh_, cfg_.mask_dilation, canvas_pitch_, T, gate_d_.p));
     PROF(DFX_FAM_INPUT, launch_input_apply(C, s, aligned_d_.p, cov_d_.p, gate_d_.p, in_acc_, in_trunc_, in_pkt_, canvas_pitch_));
+    }
 
     // layers in topological order (engine.cpp:247-281)
     for (int idx2 : net_.topo) {

@@ -364,6 +364,138 @@ __global__ void k_input_apply(Ctx c, const float* __restrict__ aligned, const ui
     }
 }
 
+// ---- fused input stage (no ROI factor, no noise filter): two launches ----
+// A: per canvas tile (grid-stride, one CTA per tile): aligned pixels
+// (alignment.cpp:106-166, same arithmetic as k_align), coverage (:179-183) and
+// per-pixel significance (engine.cpp:119-139) in one pass: each thread keeps
+// its pixels' candidate maxima for both coverage outcomes and picks one once
+// the tile's coverage is known.
+__global__ void k_input_tile_a(Ctx c, const float* __restrict__ frame, const float* __restrict__ warped,
+                               const uint8_t* __restrict__ fp, int C, float* __restrict__ aligned, int pitch, int T,
+                               BufDev acc, BufDev trunc, float thr, uint8_t* __restrict__ cov,
+                               uint8_t* __restrict__ sig) {
+    pdl_enter();
+    const FrameDev& F = *c.f;
+    const int H = F.frame_h, W = F.frame_w;
+    const size_t plane = (size_t)H * W;
+    const int T2 = T * T;
+    for (int ti = blockIdx.x; ti < F.th * F.tw; ti += gridDim.x) {
+        const int tr = ti / F.tw, tc = ti - tr * F.tw;
+        const float* ab = tile_ptr(c, F, acc, tr, tc);
+        const float* tb = tile_ptr(c, F, trunc, tr, tc);
+        int any = 0;
+        uint32_t hit_c = 0, hit_u = 0;  // per pixel slot (<= 32 pixels per thread): significant if covered / not
+        for (int p = threadIdx.x, slot = 0; p < T2; p += blockDim.x, ++slot) {
+            const int py = p / T, px = p - py * T;
+            const int cy = tr * T + py, cx = tc * T + px;
+            const int y = cy + F.sy0, x = cx + F.sx0;
+            float* dst = aligned + ((size_t)cy * pitch + cx) * C;
+            const bool inf = y >= 0 && y < H && x >= 0 && x < W;
+            bool ok = inf;
+            float mc = 0.0f, mu = 0.0f;
+            const float* a = ab + (size_t)p * C;
+            const float* t = tb + (size_t)p * C;
+            for (int ch = 0; ch < C; ++ch) {
+                float v = 0.0f;
+                if (inf && F.integer_path) {
+                    const int sy = y - F.idy, sx = x - F.idx;
+                    const bool in2 = sy >= 0 && sy < H && sx >= 0 && sx < W;
+                    if (ch == 0) ok = in2;
+                    v = in2 ? frame[(size_t)ch * plane + (size_t)sy * W + sx] : 0.0f;
+                } else if (inf) {
+                    if (ch == 0) ok = fp[(size_t)y * W + x] != 0;
+                    v = warped[(size_t)ch * plane + (size_t)y * W + x];
+                }
+                dst[ch] = v;
+                const float tv = t[ch];
+                mc = fmaxf(mc, fabsf(__fadd_rn(tv, __fsub_rn(v, a[ch]))));
+                mu = fmaxf(mu, fabsf(__fadd_rn(tv, 0.0f)));
+            }
+            any |= ok ? 1 : 0;
+            if (mc > thr) hit_c |= 1u << (slot & 31);
+            if (mu > thr) hit_u |= 1u << (slot & 31);
+        }
+        const bool covered = __syncthreads_or(any) != 0;
+        if (threadIdx.x == 0) cov[ti] = covered ? 1 : 0;
+        const uint32_t hit = covered ? hit_c : hit_u;
+        for (int p = threadIdx.x, slot = 0; p < T2; p += blockDim.x, ++slot) {
+            const int py = p / T, px = p - py * T;
+            sig[(size_t)(tr * T + py) * pitch + tc * T + px] = (hit >> (slot & 31)) & 1u;
+        }
+    }
+}
+
+// B: per tile: gate (engine.cpp:160-180, as k_gate) and the input
+// truncation (as k_input_apply) in one launch.
+__global__ void k_input_tile_b(Ctx c, const float* __restrict__ aligned, const uint8_t* __restrict__ cov,
+                               const uint8_t* __restrict__ sig, const uint8_t* __restrict__ fresh, int r, int pitch,
+                               BufDev acc, BufDev trunc, PktDev out) {
+    pdl_enter();
+    const FrameDev& F = *c.f;
+    const int T = acc.t, C = acc.C;
+    const int eh = F.th * T, ew = F.tw * T;
+    for (int ti = blockIdx.x; ti < F.th * F.tw; ti += gridDim.x) {
+        const int tr = ti / F.tw, tc = ti - tr * F.tw;
+        const bool covered = cov[ti] != 0;
+        int any = 0;
+        if (covered) {
+            any = fresh[ti] != 0;
+            const int y0 = max(tr * T - r, 0), y1 = min((tr + 1) * T + r, eh);
+            const int x0 = max(tc * T - r, 0), x1 = min((tc + 1) * T + r, ew);
+            const int w = x1 - x0, n = (y1 - y0) * w;
+            for (int p = threadIdx.x; p < n && !any; p += blockDim.x)
+                if (sig[(size_t)(y0 + p / w) * pitch + x0 + p % w]) any = 1;
+        }
+        any = __syncthreads_or(any);
+        const bool masked = covered && holds(c, F, tr, tc);
+        const bool fire = masked && any;
+        if (threadIdx.x == 0) out.ext[ext_idx(out, tr, tc)] = fire ? 1 : 0;
+        if (!masked) continue;
+        float* a = tile_ptr(c, F, acc, tr, tc);
+        float* t = tile_ptr(c, F, trunc, tr, tc);
+        const int row_len = T * C;
+        if ((row_len & 3) == 0) {
+            const int rl4 = row_len / 4;
+            for (int e = threadIdx.x; e < T * rl4; e += blockDim.x) {
+                const int yy = e / rl4, q = e - yy * rl4;
+                float4* a4 = reinterpret_cast<float4*>(a + (size_t)yy * row_len) + q;
+                float4* t4 = reinterpret_cast<float4*>(t + (size_t)yy * row_len) + q;
+                const float4 al = reinterpret_cast<const float4*>(aligned + ((size_t)(tr * T + yy) * pitch + tc * T) * C)[q];
+                const float4 av = *a4, tv = *t4;
+                const float4 raw = make_float4(__fsub_rn(al.x, av.x), __fsub_rn(al.y, av.y), __fsub_rn(al.z, av.z),
+                                               __fsub_rn(al.w, av.w));
+                const float4 cd = make_float4(__fadd_rn(tv.x, raw.x), __fadd_rn(tv.y, raw.y), __fadd_rn(tv.z, raw.z),
+                                              __fadd_rn(tv.w, raw.w));
+                if (fire) {
+                    *a4 = make_float4(__fadd_rn(av.x, cd.x), __fadd_rn(av.y, cd.y), __fadd_rn(av.z, cd.z),
+                                      __fadd_rn(av.w, cd.w));
+                    *t4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    reinterpret_cast<float4*>(out.d + pkt_off(out, tr * T + yy, tc * T))[q] = cd;
+                } else {
+                    *t4 = cd;
+                }
+            }
+        } else {
+            for (int e = threadIdx.x; e < T * row_len; e += blockDim.x) {
+                const int yy = e / row_len, rem = e - yy * row_len;
+                const size_t bi = (size_t)yy * row_len + rem;
+                const float al = aligned[((size_t)(tr * T + yy) * pitch + tc * T) * C + rem];
+                const float av = a[bi], tv = t[bi];
+                const float raw = __fsub_rn(al, av);
+                if (fire) {
+                    const float cand = __fadd_rn(tv, raw);
+                    a[bi] = __fadd_rn(av, cand);
+                    t[bi] = 0.0f;
+                    out.d[pkt_off(out, tr * T + yy, tc * T) + rem] = cand;
+                } else {
+                    t[bi] = __fadd_rn(tv, raw);
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // Claimed tiles of every buffer: zero, or the bias-init fill for truncated
 // buffers (buffer_manager.cpp:68-89, engine.cpp:78-91; fill after zero == fill).
 // Persistent grid-stride over (buffer, claim, element) with 16-byte stores.
@@ -1260,6 +1392,17 @@ void launch_align(const Ctx& c, cudaStream_t s, const float* frame, const float*
                   float* aligned, uint8_t* valid, int pitch, int T) {
     launch_pdl(k_align, persistent_grid((long long)c.rows * T * pitch), kThreads, 0, s, c, frame, warped, fp, C, aligned,
                                                                                valid, pitch, T);
+}
+void launch_input_tile_a(const Ctx& c, cudaStream_t s, const float* frame, const float* warped, const uint8_t* fp,
+                         int C, float* aligned, int pitch, int T, BufDev acc, BufDev trunc, float thr, uint8_t* cov,
+                         uint8_t* sig) {
+    launch_pdl(k_input_tile_a, num_sms_cached() * 8, kThreads, 0, s, c, frame, warped, fp, C, aligned, pitch, T, acc,
+               trunc, thr, cov, sig);
+}
+void launch_input_tile_b(const Ctx& c, cudaStream_t s, const float* aligned, const uint8_t* cov, const uint8_t* sig,
+                         const uint8_t* fresh, int dilation, int pitch, BufDev acc, BufDev trunc, PktDev out) {
+    launch_pdl(k_input_tile_b, num_sms_cached() * 8, kThreads, 0, s, c, aligned, cov, sig, fresh, dilation, pitch, acc,
+               trunc, out);
 }
 void launch_count_dropped(const Ctx& c, cudaStream_t s, const uint8_t* fp, int T, unsigned long long* counter) {
     launch_pdl(k_count_dropped, num_sms_cached() * 4, kThreads, 0, s, c, fp, T, counter);

@@ -136,6 +136,13 @@ struct Readback {  // copied by the last kernel of a frame into mapped host memo
     unsigned out_val = 0;
 };
 void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out, Readback rb);
+// Fused input stage (no ROI factor, no noise filter): A = align + coverage +
+// significance per canvas tile, B = gate + input truncation per tile.
+void launch_input_tile_a(const Ctx& c, cudaStream_t s, const float* frame, const float* warped, const uint8_t* fp,
+                         int C, float* aligned, int pitch, int T, BufDev acc, BufDev trunc, float thr, uint8_t* cov,
+                         uint8_t* sig);
+void launch_input_tile_b(const Ctx& c, cudaStream_t s, const float* aligned, const uint8_t* cov, const uint8_t* sig,
+                         const uint8_t* fresh, int dilation, int pitch, BufDev acc, BufDev trunc, PktDev out);
 // First kernel of a frame: parameter block (mapped host -> device slot), counters zeroed, host ack.
 void launch_frame_begin(cudaStream_t s, const void* src, void* dst, size_t bytes, void* counters, size_t cnt_bytes,
                         unsigned* ack, unsigned seq, const unsigned* in_flag = nullptr, unsigned in_val = 0);
