@@ -706,13 +706,17 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     PROF(DFX_FAM_CLAIMS, launch_claims(C, s, d_claims_, claim_bufs_.p, nclaim_bufs_, max_claims_));
 
     // input stage
-    if (!integer) PROF(DFX_FAM_INPUT, launch_warp(C, s, frame_dev, c, warped_d_.p, fp_d_.p));
-    if (cropped && !integer) PROF(DFX_FAM_INPUT, launch_count_dropped(C, s, fp_d_.p, T, dropped));
     static const bool fuse_input = !(getenv("DFX_FUSE_INPUT") && getenv("DFX_FUSE_INPUT")[0] == '0');
-    if (fuse_input && !F.roi && !cfg_.noise_suppression) {
+    const bool fused_in = fuse_input && !F.roi && !cfg_.noise_suppression;
+    // the fused stage samples the frame itself unless the crop count needs k_warp's full-frame map
+    const bool direct = fused_in && !integer && !cropped;
+    if (!integer && !direct) PROF(DFX_FAM_INPUT, launch_warp(C, s, frame_dev, c, warped_d_.p, fp_d_.p));
+    if (cropped && !integer) PROF(DFX_FAM_INPUT, launch_count_dropped(C, s, fp_d_.p, T, dropped));
+    if (fused_in) {
         // two launches: align + coverage + significance, then gate + input truncation
         PROF(DFX_FAM_INPUT, launch_input_tile_a(C, s, frame_dev, warped_d_.p, fp_d_.p, c, aligned_d_.p, canvas_pitch_, T,
-                                                in_acc_, in_trunc_, cfg_.input_threshold, cov_d_.p, sig_d_.p));
+                                                in_acc_, in_trunc_, cfg_.input_threshold, cov_d_.p, sig_d_.p,
+                                                direct ? 1 : 0));
         PROF(DFX_FAM_INPUT, launch_input_tile_b(C, s, aligned_d_.p, cov_d_.p, sig_d_.p, d_fresh_, cfg_.mask_dilation,
                                                 canvas_pitch_, in_acc_, in_trunc_, in_pkt_));
     } else {

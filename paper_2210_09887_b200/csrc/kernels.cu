@@ -69,7 +69,35 @@ int grid_for(long long n, int per_block = kThreads) {
 }
 
 // ----------------------------------------------------------------- warp
-// alignment.cpp:58-104, bilinear branch: inverse mapping in double, float weights.
+// alignment.cpp:58-104, bilinear branch: inverse mapping in double, float
+// weights. Source position of frame pixel (x, y); false if outside the frame.
+struct WarpTap {
+    int x0, y0, x1, y1;
+    float fx, fy, gx, gy;
+};
+__device__ __forceinline__ bool warp_tap(const FrameDev& F, int x, int y, WarpTap& w4) {
+    const int H = F.frame_h, W = F.frame_w;
+    const double xd = x, yd = y;
+    const double w = __dadd_rn(__dadd_rn(__dmul_rn((double)F.inv[6], xd), __dmul_rn((double)F.inv[7], yd)),
+                               (double)F.inv[8]);
+    const double sx = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn((double)F.inv[0], xd), __dmul_rn((double)F.inv[1], yd)),
+                                          (double)F.inv[2]), w);
+    const double sy = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn((double)F.inv[3], xd), __dmul_rn((double)F.inv[4], yd)),
+                                          (double)F.inv[5]), w);
+    if (sx < 0.0 || sx > W - 1 || sy < 0.0 || sy > H - 1) return false;
+    w4.x0 = (int)floor(sx), w4.y0 = (int)floor(sy);
+    w4.fx = (float)(sx - w4.x0), w4.fy = (float)(sy - w4.y0);
+    w4.x1 = min(w4.x0 + 1, W - 1), w4.y1 = min(w4.y0 + 1, H - 1);
+    w4.gx = __fsub_rn(1.0f, w4.fx), w4.gy = __fsub_rn(1.0f, w4.fy);
+    return true;
+}
+__device__ __forceinline__ float warp_sample(const float* p, int W, const WarpTap& w4) {
+    const float v00 = p[(size_t)w4.y0 * W + w4.x0], v01 = p[(size_t)w4.y0 * W + w4.x1];
+    const float v10 = p[(size_t)w4.y1 * W + w4.x0], v11 = p[(size_t)w4.y1 * W + w4.x1];
+    const float top = __fadd_rn(__fmul_rn(w4.gx, v00), __fmul_rn(w4.fx, v01));
+    const float bot = __fadd_rn(__fmul_rn(w4.gx, v10), __fmul_rn(w4.fx, v11));
+    return __fadd_rn(__fmul_rn(w4.gy, top), __fmul_rn(w4.fy, bot));
+}
 __global__ void k_warp(Ctx c, const float* __restrict__ frame, int C, float* __restrict__ warped,
                        uint8_t* __restrict__ fp) {
     pdl_enter();
@@ -78,31 +106,10 @@ __global__ void k_warp(Ctx c, const float* __restrict__ frame, int C, float* __r
     const long long n = (long long)H * W;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const int y = (int)(i / W), x = (int)(i % W);
-        const double xd = x, yd = y;
-        const double w = __dadd_rn(__dadd_rn(__dmul_rn((double)F.inv[6], xd), __dmul_rn((double)F.inv[7], yd)),
-                                   (double)F.inv[8]);
-        const double sx = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn((double)F.inv[0], xd), __dmul_rn((double)F.inv[1], yd)),
-                                              (double)F.inv[2]), w);
-        const double sy = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn((double)F.inv[3], xd), __dmul_rn((double)F.inv[4], yd)),
-                                              (double)F.inv[5]), w);
-        const bool ok = !(sx < 0.0 || sx > W - 1 || sy < 0.0 || sy > H - 1);
+        WarpTap w4;
+        const bool ok = warp_tap(F, x, y, w4);
         fp[i] = ok ? 1 : 0;
-        if (!ok) {
-            for (int ch = 0; ch < C; ++ch) warped[(size_t)ch * n + i] = 0.0f;
-            continue;
-        }
-        const int x0 = (int)floor(sx), y0 = (int)floor(sy);
-        const float fx = (float)(sx - x0), fy = (float)(sy - y0);
-        const int x1 = min(x0 + 1, W - 1), y1 = min(y0 + 1, H - 1);
-        const float gx = __fsub_rn(1.0f, fx), gy = __fsub_rn(1.0f, fy);
-        for (int ch = 0; ch < C; ++ch) {
-            const float* p = frame + (size_t)ch * n;
-            const float v00 = p[(size_t)y0 * W + x0], v01 = p[(size_t)y0 * W + x1];
-            const float v10 = p[(size_t)y1 * W + x0], v11 = p[(size_t)y1 * W + x1];
-            const float top = __fadd_rn(__fmul_rn(gx, v00), __fmul_rn(fx, v01));
-            const float bot = __fadd_rn(__fmul_rn(gx, v10), __fmul_rn(fx, v11));
-            warped[(size_t)ch * n + i] = __fadd_rn(__fmul_rn(gy, top), __fmul_rn(fy, bot));
-        }
+        for (int ch = 0; ch < C; ++ch) warped[(size_t)ch * n + i] = ok ? warp_sample(frame + (size_t)ch * n, W, w4) : 0.0f;
     }
 }
 
@@ -373,7 +380,7 @@ __global__ void k_input_apply(Ctx c, const float* __restrict__ aligned, const ui
 __global__ void k_input_tile_a(Ctx c, const float* __restrict__ frame, const float* __restrict__ warped,
                                const uint8_t* __restrict__ fp, int C, float* __restrict__ aligned, int pitch, int T,
                                BufDev acc, BufDev trunc, float thr, uint8_t* __restrict__ cov,
-                               uint8_t* __restrict__ sig) {
+                               uint8_t* __restrict__ sig, int direct) {
     pdl_enter();
     const FrameDev& F = *c.f;
     const int H = F.frame_h, W = F.frame_w;
@@ -395,6 +402,9 @@ __global__ void k_input_tile_a(Ctx c, const float* __restrict__ frame, const flo
             float mc = 0.0f, mu = 0.0f;
             const float* a = ab + (size_t)p * C;
             const float* t = tb + (size_t)p * C;
+            WarpTap w4;
+            bool wok = false;
+            if (direct && inf) wok = warp_tap(F, x, y, w4);  // bilinear sample straight from the frame
             for (int ch = 0; ch < C; ++ch) {
                 float v = 0.0f;
                 if (inf && F.integer_path) {
@@ -402,6 +412,9 @@ __global__ void k_input_tile_a(Ctx c, const float* __restrict__ frame, const flo
                     const bool in2 = sy >= 0 && sy < H && sx >= 0 && sx < W;
                     if (ch == 0) ok = in2;
                     v = in2 ? frame[(size_t)ch * plane + (size_t)sy * W + sx] : 0.0f;
+                } else if (inf && direct) {
+                    if (ch == 0) ok = wok;
+                    v = wok ? warp_sample(frame + (size_t)ch * plane, W, w4) : 0.0f;
                 } else if (inf) {
                     if (ch == 0) ok = fp[(size_t)y * W + x] != 0;
                     v = warped[(size_t)ch * plane + (size_t)y * W + x];
@@ -1395,9 +1408,9 @@ void launch_align(const Ctx& c, cudaStream_t s, const float* frame, const float*
 }
 void launch_input_tile_a(const Ctx& c, cudaStream_t s, const float* frame, const float* warped, const uint8_t* fp,
                          int C, float* aligned, int pitch, int T, BufDev acc, BufDev trunc, float thr, uint8_t* cov,
-                         uint8_t* sig) {
+                         uint8_t* sig, int direct) {
     launch_pdl(k_input_tile_a, num_sms_cached() * 8, kThreads, 0, s, c, frame, warped, fp, C, aligned, pitch, T, acc,
-               trunc, thr, cov, sig);
+               trunc, thr, cov, sig, direct);
 }
 void launch_input_tile_b(const Ctx& c, cudaStream_t s, const float* aligned, const uint8_t* cov, const uint8_t* sig,
                          const uint8_t* fresh, int dilation, int pitch, BufDev acc, BufDev trunc, PktDev out) {

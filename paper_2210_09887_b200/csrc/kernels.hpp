@@ -140,7 +140,7 @@ void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, floa
 // significance per canvas tile, B = gate + input truncation per tile.
 void launch_input_tile_a(const Ctx& c, cudaStream_t s, const float* frame, const float* warped, const uint8_t* fp,
                          int C, float* aligned, int pitch, int T, BufDev acc, BufDev trunc, float thr, uint8_t* cov,
-                         uint8_t* sig);
+                         uint8_t* sig, int direct);  // direct: bilinear samples computed from the frame (no k_warp)
 void launch_input_tile_b(const Ctx& c, cudaStream_t s, const float* aligned, const uint8_t* cov, const uint8_t* sig,
                          const uint8_t* fresh, int dilation, int pitch, BufDev acc, BufDev trunc, PktDev out);
 // First kernel of a frame: parameter block (mapped host -> device slot), counters zeroed, host ack.
