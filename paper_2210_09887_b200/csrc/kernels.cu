@@ -405,24 +405,40 @@ __global__ void k_input_tile_a(Ctx c, const float* __restrict__ frame, const flo
             WarpTap w4;
             bool wok = false;
             if (direct && inf) wok = warp_tap(F, x, y, w4);  // bilinear sample straight from the frame
-            for (int ch = 0; ch < C; ++ch) {
-                float v = 0.0f;
-                if (inf && F.integer_path) {
-                    const int sy = y - F.idy, sx = x - F.idx;
-                    const bool in2 = sy >= 0 && sy < H && sx >= 0 && sx < W;
-                    if (ch == 0) ok = in2;
-                    v = in2 ? frame[(size_t)ch * plane + (size_t)sy * W + sx] : 0.0f;
-                } else if (inf && direct) {
-                    if (ch == 0) ok = wok;
-                    v = wok ? warp_sample(frame + (size_t)ch * plane, W, w4) : 0.0f;
-                } else if (inf) {
-                    if (ch == 0) ok = fp[(size_t)y * W + x] != 0;
-                    v = warped[(size_t)ch * plane + (size_t)y * W + x];
+            int sy = 0, sx = 0;
+            if (inf && F.integer_path) {
+                sy = y - F.idy, sx = x - F.idx;
+                ok = sy >= 0 && sy < H && sx >= 0 && sx < W;
+            } else if (inf && direct) {
+                ok = wok;
+            } else if (inf) {
+                ok = fp[(size_t)y * W + x] != 0;
+            }
+            // 4 channels at a time: every load of the group issued before any use
+            for (int c0 = 0; c0 < C; c0 += 4) {
+                float v[4], av[4], tv[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int ch = c0 + q;
+                    v[q] = 0.0f, av[q] = 0.0f, tv[q] = 0.0f;
+                    if (ch >= C) continue;
+                    if (inf && F.integer_path) {
+                        if (ok) v[q] = frame[(size_t)ch * plane + (size_t)sy * W + sx];
+                    } else if (inf && direct) {
+                        if (wok) v[q] = warp_sample(frame + (size_t)ch * plane, W, w4);
+                    } else if (inf) {
+                        v[q] = warped[(size_t)ch * plane + (size_t)y * W + x];
+                    }
+                    av[q] = a[ch];
+                    tv[q] = t[ch];
                 }
-                dst[ch] = v;
-                const float tv = t[ch];
-                mc = fmaxf(mc, fabsf(__fadd_rn(tv, __fsub_rn(v, a[ch]))));
-                mu = fmaxf(mu, fabsf(__fadd_rn(tv, 0.0f)));
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (c0 + q >= C) continue;
+                    dst[c0 + q] = v[q];
+                    mc = fmaxf(mc, fabsf(__fadd_rn(tv[q], __fsub_rn(v[q], av[q]))));
+                    mu = fmaxf(mu, fabsf(__fadd_rn(tv[q], 0.0f)));
+                }
             }
             any |= ok ? 1 : 0;
             if (mc > thr) hit_c |= 1u << (slot & 31);
@@ -456,8 +472,16 @@ __global__ void k_input_tile_b(Ctx c, const float* __restrict__ aligned, const u
             const int y0 = max(tr * T - r, 0), y1 = min((tr + 1) * T + r, eh);
             const int x0 = max(tc * T - r, 0), x1 = min((tc + 1) * T + r, ew);
             const int w = x1 - x0, n = (y1 - y0) * w;
-            for (int p = threadIdx.x; p < n && !any; p += blockDim.x)
-                if (sig[(size_t)(y0 + p / w) * pitch + x0 + p % w]) any = 1;
+            // up to 4 window bytes per thread per round, loaded together
+            for (int p0 = threadIdx.x; p0 < n; p0 += 4 * blockDim.x) {
+                uint8_t sv[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int p = p0 + q * blockDim.x;
+                    sv[q] = p < n ? sig[(size_t)(y0 + p / w) * pitch + x0 + p % w] : 0;
+                }
+                any |= (sv[0] | sv[1] | sv[2] | sv[3]) != 0;
+            }
         }
         any = __syncthreads_or(any);
         const bool masked = covered && holds(c, F, tr, tc);
