@@ -1348,23 +1348,36 @@ __global__ void k_densify8(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ 
     for (int it = gw; it < G * oh; it += nw) {
         const int g = it / oh, y = it - g * oh;
         const int qy = y / t, yy = y - qy * t;
-        for (int x = lane; x < ow; x += 32) {
-            const int qx = x / t;
-            const size_t off = (size_t)slot_of(F, c.rows, c.cols, qy, qx) * t * t * C +
-                               ((size_t)yy * t + (x - qx * t)) * C + g * 8;
-            const float4 a0 = __ldcs(reinterpret_cast<const float4*>(acc.d + off));
-            const float4 a1 = __ldcs(reinterpret_cast<const float4*>(acc.d + off) + 1);
-            const float4 t0 = __ldcs(reinterpret_cast<const float4*>(trunc.d + off));
-            const float4 t1 = __ldcs(reinterpret_cast<const float4*>(trunc.d + off) + 1);
-            float* o = out + (size_t)(g * 8) * plane + (size_t)y * ow + x;
-            o[0] = __fadd_rn(a0.x, t0.x);
-            o[plane] = __fadd_rn(a0.y, t0.y);
-            o[2 * plane] = __fadd_rn(a0.z, t0.z);
-            o[3 * plane] = __fadd_rn(a0.w, t0.w);
-            o[4 * plane] = __fadd_rn(a1.x, t1.x);
-            o[5 * plane] = __fadd_rn(a1.y, t1.y);
-            o[6 * plane] = __fadd_rn(a1.z, t1.z);
-            o[7 * plane] = __fadd_rn(a1.w, t1.w);
+        // two pixels per lane per round, all 8 loads issued before any use
+        for (int x0 = lane; x0 < ow; x0 += 64) {
+            float4 a0[2], a1[2], t0[2], t1[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int x = x0 + 32 * u;
+                if (x < ow) {
+                    const int qx = x / t;
+                    const size_t off = (size_t)slot_of(F, c.rows, c.cols, qy, qx) * t * t * C +
+                                       ((size_t)yy * t + (x - qx * t)) * C + g * 8;
+                    a0[u] = __ldcs(reinterpret_cast<const float4*>(acc.d + off));
+                    a1[u] = __ldcs(reinterpret_cast<const float4*>(acc.d + off) + 1);
+                    t0[u] = __ldcs(reinterpret_cast<const float4*>(trunc.d + off));
+                    t1[u] = __ldcs(reinterpret_cast<const float4*>(trunc.d + off) + 1);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int x = x0 + 32 * u;
+                if (x >= ow) continue;
+                float* o = out + (size_t)(g * 8) * plane + (size_t)y * ow + x;
+                o[0] = __fadd_rn(a0[u].x, t0[u].x);
+                o[plane] = __fadd_rn(a0[u].y, t0[u].y);
+                o[2 * plane] = __fadd_rn(a0[u].z, t0[u].z);
+                o[3 * plane] = __fadd_rn(a0[u].w, t0[u].w);
+                o[4 * plane] = __fadd_rn(a1[u].x, t1[u].x);
+                o[5 * plane] = __fadd_rn(a1[u].y, t1[u].y);
+                o[6 * plane] = __fadd_rn(a1[u].z, t1[u].z);
+                o[7 * plane] = __fadd_rn(a1[u].w, t1[u].w);
+            }
         }
     }
     if (trace) {
