@@ -1,10 +1,10 @@
 // Conv planning block (target bits, exact output TileMask, FLOP pixels, dense
-// unit / tile list, gathered list, zero fill), shared by k_conv_plan
-// (conv_dense.cu) and the activation kernels that run the next conv's plan
-// (measured: running it inside a persistent kernel loses to the standalone
-// launch; plan blocks need many resident CTAs). Textually included INSIDE each
-// translation unit's anonymous namespace (every TU gets its own copy); the
-// includer provides kernels.hpp / dfx_types.hpp.
+// unit / tile list, gathered list, zero fill) of k_conv_plan, as a block
+// function over PlanArgs so other kernels can embed it (measured on C2:
+// running it inside the persistent dense-conv or activation kernels loses to
+// the standalone launch, plan blocks need many resident CTAs). Textually
+// included INSIDE the translation unit's anonymous namespace; the includer
+// provides kernels.hpp / dfx_types.hpp.
 #pragma once
 
 constexpr int kUY = 16, kUX = 8;  // unit = 16 rows x 8 cols = 128 pixels
