@@ -25,6 +25,9 @@ namespace dfx {
 
 namespace {
 
+#ifndef DFX_TRUNC_MINB  // CTAs per SM of k_trunc_coop (measured: 3 -> 80 registers with spills, slower)
+#define DFX_TRUNC_MINB 2
+#endif
 constexpr int kSub = 8;               // float4s per lane in flight per array
 constexpr int kChunkF4 = 32 * kSub;
 #ifndef DFX_TRUNC_PREFETCH
@@ -371,7 +374,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr) {
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_trunc_coop(Ctx c, PktDev in, BufDev acc, BufDev trunc,
+__global__ void __launch_bounds__(256, DFX_TRUNC_MINB) k_trunc_coop(Ctx c, PktDev in, BufDev acc, BufDev trunc,
                                                     unsigned* __restrict__ tile_max, float thr, int relu, PktDev out,
                                                     unsigned* __restrict__ gbar, unsigned long long* tr, int dry) {
     tstamp(tr, 0);
