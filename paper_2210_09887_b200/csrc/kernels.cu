@@ -603,11 +603,32 @@ __global__ void k_claims(Ctx c, const int* __restrict__ claim_slots, const Claim
     }
     const FrameDev& F = *c.f;
     const int nq = F.nclaims;
+    if (nq == 0) return;
+    // the buffer descriptors in shared memory first (one round of loads, not
+    // one dependent global load per buffer in the loop below)
+    constexpr int kMaxBufs = 128;
+    __shared__ ClaimBuf s_bufs[kMaxBufs];
+    for (int i = threadIdx.x; i < nbuf && i < kMaxBufs; i += blockDim.x) s_bufs[i] = bufs[i];
+    __syncthreads();
     const long long tid0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, nthr = (long long)gridDim.x * blockDim.x;
     for (int bi = 0; bi < nbuf; ++bi) {
-        const ClaimBuf b = bufs[bi];
+        const ClaimBuf b = bi < kMaxBufs ? s_bufs[bi] : bufs[bi];
         const long long n = (long long)b.t * b.t * b.C;  // floats per tile
-        if ((b.C & 3) == 0) {
+        if ((b.C & 3) == 0 && (long long)nq * (n / 4) < (1LL << 31)) {
+            // 32-bit indices; shifts when the tile's float4 count / channel count are powers of two
+            const int n4 = (int)(n / 4), tot = nq * n4, c4 = b.C / 4;
+            const bool p2 = (n4 & (n4 - 1)) == 0 && (c4 & (c4 - 1)) == 0;
+            const int sh = p2 ? __ffs(n4) - 1 : 0;
+            for (int e = (int)tid0; e < tot; e += (int)nthr) {
+                const int ci = p2 ? (e >> sh) : e / n4, r = e - ci * n4;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (b.fill) {
+                    const int ch = 4 * (p2 ? (r & (c4 - 1)) : r % c4);
+                    v = make_float4(b.fill[ch], b.fill[ch + 1], b.fill[ch + 2], b.fill[ch + 3]);
+                }
+                reinterpret_cast<float4*>(b.d + (size_t)claim_slots[ci] * n)[r] = v;
+            }
+        } else if ((b.C & 3) == 0) {
             const long long n4 = n / 4;
             for (long long e = tid0; e < (long long)nq * n4; e += nthr) {
                 const long long ci = e / n4, r = e - ci * n4;
