@@ -169,20 +169,46 @@ __device__ void plan_block(const Ctx& c, const PlanArgs& pa, int blk, PlanSmem& 
     const bool active_tile = __syncthreads_or(threadIdx.x < ntl && s_tstore[threadIdx.x]);
     if ((nun > 1 || tau > 1) && sparse_unit && active_tile) {
         const int C = out.C;
-        const int per = (C & 3) == 0 ? C / 4 : C;
-        const FDiv dper(per);
-        for (int e = threadIdx.x; e < npx * per; e += NT) {
-            const int p = dper(e), q = e - p * per;
-            const int ly = dbw(p), lx = p - ly * BW;
-            if (s_ucnt[(ly / kUY) * upr + lx / kUX] >= tau || !s_tstore[dt(ly) * tpr + dt(lx)] ||
-                ((s_bits[p >> 5] >> (p & 31)) & 1u))
-                continue;
-            const int y = Y0 + ly, x = X0 + lx;
-            if (y < -hs || y >= eh + hs || x < -hs || x >= ew + hs) continue;
-            if ((C & 3) == 0)
-                reinterpret_cast<float4*>(out.d + pkt_off(out, y, x))[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-            else
+        if ((C & 3) == 0) {
+            // warp-cooperative: each warp ballots which of its 32 pixels need zeros,
+            // then writes two pixels' float4 rows per instruction (coalesced)
+            const int C4 = C / 4, lane = threadIdx.x & 31;
+            for (int p0 = (threadIdx.x & ~31); p0 < npx; p0 += NT) {
+                const int p = p0 + lane;
+                bool z = false;
+                int y = 0, x = 0;
+                if (p < npx) {
+                    const int ly = dbw(p), lx = p - ly * BW;
+                    y = Y0 + ly, x = X0 + lx;
+                    z = s_ucnt[(ly / kUY) * upr + lx / kUX] < tau && s_tstore[dt(ly) * tpr + dt(lx)] &&
+                        !((s_bits[p >> 5] >> (p & 31)) & 1u) && y >= -hs && y < eh + hs && x >= -hs && x < ew + hs;
+                }
+                unsigned m = __ballot_sync(0xffffffffu, z);
+                while (m) {
+                    const int a0 = __ffs(m) - 1;
+                    m &= m - 1;
+                    int a1 = -1;
+                    if (m) a1 = __ffs(m) - 1, m &= m - 1;
+                    const int src = lane < 16 ? a0 : a1;
+                    const int yy = __shfl_sync(0xffffffffu, y, src < 0 ? 0 : src);
+                    const int xx = __shfl_sync(0xffffffffu, x, src < 0 ? 0 : src);
+                    if (src >= 0) {
+                        float4* row = reinterpret_cast<float4*>(out.d + pkt_off(out, yy, xx));
+                        for (int q = lane & 15; q < C4; q += 16) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
+            }
+        } else {
+            for (int e = threadIdx.x; e < npx * C; e += NT) {
+                const int p = e / C, q = e - p * C;
+                const int ly = dbw(p), lx = p - ly * BW;
+                if (s_ucnt[(ly / kUY) * upr + lx / kUX] >= tau || !s_tstore[dt(ly) * tpr + dt(lx)] ||
+                    ((s_bits[p >> 5] >> (p & 31)) & 1u))
+                    continue;
+                const int y = Y0 + ly, x = X0 + lx;
+                if (y < -hs || y >= eh + hs || x < -hs || x >= ew + hs) continue;
                 out.d[pkt_off(out, y, x) + q] = 0.0f;
+            }
         }
     }
 }
