@@ -356,6 +356,80 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
         kb1 = (int)(((long long)nKB * (ks + 1)) / S);
     };
 
+    // Patch loading (loader warps, and every thread in the prologue below):
+    // per-pixel source offsets (-1: zero) of an item's patches, then one
+    // channel chunk of the raw fp32 patch with cp.async (zero fill via src-size 0).
+    const int c4n = KC / 4;
+    const int P = a.ppx;  // patch pixels per unit
+    const int E1 = P * c4n;
+    const bool vec = (a.in.C & 3) == 0;
+    auto patch_offsets = [&](int pr, int nu, int t0, int stride) {
+        int y0[2] = {0, 0}, x0[2] = {0, 0};
+        if (!a.tpu) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int uv = __ldcg(a.units + UPI * pr + (j < nu ? j : 0));
+                y0[j] = ((uv >> 16) - 1) * kUY - a.r;
+                x0[j] = ((uv & 0xffff) - 1) * kUX - a.r;
+            }
+        }
+        for (int q = t0; q < P * nu; q += stride) {
+            const int j = q >= P ? 1 : 0, p = q - j * P;
+            int y, x;
+            bool ok = true;
+            if (a.tpu) {  // tile s of the unit, (T + 2r)^2-pixel patch per tile
+                const int s = p / (PW * PW), l = p - s * PW * PW;
+                const int py = l / PW, px = l - py * PW;
+                const int li = pr * a.tpu + s;
+                ok = li < listed;
+                const int tv = ok ? __ldcg(a.units + li) : 0;
+                y = (((tv >> 16) - 8) << a.tsh) - a.r + py;
+                x = (((tv & 0xffff) - 8) << a.tsh) - a.r + px;
+            } else {
+                const int py = p / PW, px = p - py * PW;
+                y = (j ? y0[1] : y0[0]) + py, x = (j ? x0[1] : x0[0]) + px;
+            }
+            s_poff[q] = ok && pkt_ok(a.in, F.th, F.tw, y, x) ? (int)pkt_off(a.in, y, x) : -1;
+        }
+    };
+    auto copy_chunk = [&](uint32_t buf, int cbase, int nu, int t0, int stride) {
+        for (int e = t0; e < E1 * nu; e += stride) {
+            const int j = e >= E1 ? 1 : 0;
+            const int e1 = e - j * E1;
+            const int p = e1 / c4n, c4 = e1 - p * c4n;
+            const int ch = cbase + c4 * 4;
+            const uint32_t dst = buf + j * unit_bytes + p * a.pstr + c4 * 16;
+            const int off = s_poff[j * P + p];
+            const bool ok = off >= 0;
+            if (vec) {
+                const bool v = ok && ch < a.cin;
+                cp_async16(dst, v ? a.in.d + off + ch : a.in.d, v ? 16u : 0u);
+            } else {
+                const float* src = ok ? a.in.d + off : a.in.d;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const bool v = ok && ch + q < a.cin;
+                    cp_async4(dst + 4 * q, v ? src + ch + q : a.in.d, v ? 4u : 0u);
+                }
+            }
+        }
+    };
+    // Prologue: the CTA's first patch (offsets + first channel chunk) is built by
+    // ALL threads, so the first MMA is not gated by 4 loader warps walking a
+    // dependent chain alone (~4-6 us per launch before).
+    {
+        int pr, nb, kb0, kb1;
+        item_info(blockIdx.x, pr, nb, kb0, kb1);
+        const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
+        patch_offsets(pr, nu, tid, kDenseThreads);
+        __syncthreads();
+        copy_chunk(sbase, (kb0 / K2) * KC, nu, tid, kDenseThreads);
+        cp_async_wait_all();
+        __syncthreads();
+        if (tid == 0)
+            for (int i = 0; i < 4; ++i) mbar_arrive(smem_u32(&bar_pf[0]));  // the 4 loader-warp arrivals
+    }
+
     if (warp < 4 * kProdWG) {
         // ------------------------------------------------ A producers (patch rows -> TMEM)
         // kProdWG warpgroups take K-blocks round robin (tcgen05.st + wait::st is
@@ -422,78 +496,30 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
             }
         }
     } else if (warp < 4 * kProdWG + 4) {
-        // ------------------------------------------------ patch loaders (cp.async, zero fill, TF32 split)
+        // ------------------------------------------------ patch loaders (cp.async, zero fill)
         const int lt = tid - 128 * kProdWG;
-        const int c4n = KC / 4;
-        const int P = a.ppx;  // patch pixels per unit
-        const int E1 = P * c4n;
-        const bool vec = (a.in.C & 3) == 0;
         uint32_t pseq = 0;
         for (int it = blockIdx.x; it < items; it += gridDim.x) {
             int pr, nb, kb0, kb1;
             item_info(it, pr, nb, kb0, kb1);
             const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
-            int y0[2] = {0, 0}, x0[2] = {0, 0};
-            if (!a.tpu) {
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const int uv = __ldcg(a.units + UPI * pr + (j < nu ? j : 0));
-                    y0[j] = ((uv >> 16) - 1) * kUY - a.r;
-                    x0[j] = ((uv & 0xffff) - 1) * kUX - a.r;
-                }
+            const bool first = it == (int)blockIdx.x;  // its offsets and first chunk came from the prologue
+            if (!first) {
+                asm volatile("bar.sync 2, 128;" ::: "memory");  // previous item's copy loop is done with s_poff
+                patch_offsets(pr, nu, lt, 128);
+                asm volatile("bar.sync 2, 128;" ::: "memory");
             }
-            const int E = E1 * nu;
-            // per-pixel source offset (-1: zero) of the item's patches, once per item:
-            // keeps the dependent ext-map lookups out of the per-chunk copy loop
-            asm volatile("bar.sync 2, 128;" ::: "memory");  // previous item's copy loop is done with s_poff
-            for (int q = lt; q < P * nu; q += 128) {
-                const int j = q >= P ? 1 : 0, p = q - j * P;
-                int y, x;
-                bool ok = true;
-                if (a.tpu) {  // tile s of the unit, (T + 2r)^2-pixel patch per tile
-                    const int s = p / (PW * PW), l = p - s * PW * PW;
-                    const int py = l / PW, px = l - py * PW;
-                    const int li = pr * a.tpu + s;
-                    ok = li < listed;
-                    const int tv = ok ? __ldcg(a.units + li) : 0;
-                    y = (((tv >> 16) - 8) << a.tsh) - a.r + py;
-                    x = (((tv & 0xffff) - 8) << a.tsh) - a.r + px;
-                } else {
-                    const int py = p / PW, px = p - py * PW;
-                    y = (j ? y0[1] : y0[0]) + py, x = (j ? x0[1] : x0[0]) + px;
-                }
-                s_poff[q] = ok && pkt_ok(a.in, F.th, F.tw, y, x) ? (int)pkt_off(a.in, y, x) : -1;
-            }
-            asm volatile("bar.sync 2, 128;" ::: "memory");
-            for (int cb = kb0 / K2; cb <= (kb1 - 1) / K2; ++cb, ++pseq) {
+            for (int cb = kb0 / K2 + (first ? 1 : 0); cb <= (kb1 - 1) / K2; ++cb) {
+                if (first && pseq == 0) pseq = 1;
                 const uint32_t pb = pseq % a.npb;
                 mbar_wait(smem_u32(&bar_pe[pb]), ((pseq / a.npb) & 1) ^ 1);
-                const uint32_t buf = sbase + pb * buf_bytes;
-                const int cbase = cb * KC;
-                for (int e = lt; e < E; e += 128) {
-                    const int j = e >= E1 ? 1 : 0;
-                    const int e1 = e - j * E1;
-                    const int p = e1 / c4n, c4 = e1 - p * c4n;
-                    const int ch = cbase + c4 * 4;
-                    const uint32_t dst = buf + j * unit_bytes + p * a.pstr + c4 * 16;
-                    const int off = s_poff[j * P + p];
-                    const bool ok = off >= 0;
-                    if (vec) {
-                        const bool v = ok && ch < a.cin;
-                        cp_async16(dst, v ? a.in.d + off + ch : a.in.d, v ? 16u : 0u);
-                    } else {
-                        const float* src = ok ? a.in.d + off : a.in.d;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const bool v = ok && ch + q < a.cin;
-                            cp_async4(dst + 4 * q, v ? src + ch + q : a.in.d, v ? 4u : 0u);
-                        }
-                    }
-                }
+                copy_chunk(sbase + pb * buf_bytes, cb * KC, nu, lt, 128);
                 cp_async_wait_all();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bar_pf[pb]));
+                ++pseq;
             }
+            if (first && pseq == 0) pseq = 1;  // single-chunk first item
         }
     } else if (warp < 4 * kProdWG + 8) {
         // ------------------------------------------------ epilogue: TMEM -> packet / split-K workspace
