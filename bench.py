@@ -39,7 +39,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 METRIC = "frames/s at named update rate on 1/8 B200; HBM GB/s & tensor-pipe % vs peak"
 TILE = 16
 FRAME = 512
-INPUT_THR = 0.3
+INPUT_THR = 2.0  # tuned so the C2 sequence runs at the named ~10% update rate over the default window
 DILATION = 4
 CPU_CROP = 128  # CPU-baseline sample: same network / camera motion on a 128x128 window
 WORKLOAD_FILE = os.path.join(ROOT, "profiles", "workload_c2.json")

@@ -184,6 +184,34 @@ def pan_rotate_sequence(rng, c, h, w, frames, pan_x, pan_y, deg_per_frame, world
     return seq
 
 
+def pan_wobble_sequence(rng, c, h, w, frames, pan_x, pan_y, deg_amp, period, obj=True, obj_v=(3, 2)):
+    """Stationary camera motion for benchmarks: constant pan plus a bounded
+    rotation wobble theta_k = deg_amp * sin(2 pi k / period) about the frame
+    centre (frame k's homography maps its pixels into world coordinates), and
+    a textured object moving in frame coordinates (wrapping around), so the
+    update rate does not drift with the sequence length."""
+    margin = int(abs(pan_x) * frames + abs(pan_y) * frames + max(h, w)) + 8
+    world = texture(rng, c, h + 2 * margin, w + 2 * margin)
+    obj_tex = texture(rng, c, 40, 40) if obj else None
+    seq = []
+    yy, xx = np.mgrid[0:h, 0:w].astype(np.float64)
+    cx, cy = (w - 1) / 2.0, (h - 1) / 2.0
+    for f in range(frames):
+        th = np.deg2rad(deg_amp * np.sin(2.0 * np.pi * f / period))
+        ct, st = np.cos(th), np.sin(th)
+        tx, ty = pan_x * f, pan_y * f
+        a, b, cc_ = ct, -st, cx - ct * cx + st * cy + tx
+        d, e, ff = st, ct, cy - st * cx - ct * cy + ty
+        H = np.array([a, b, cc_, d, e, ff, 0, 0, 1], np.float32)
+        frame = bilinear_sample(world, a * xx + b * yy + cc_ + margin, d * xx + e * yy + ff + margin)
+        if obj:
+            ox = (30 + obj_v[0] * f) % (w - 40)
+            oy = (20 + obj_v[1] * f) % (h - 40)
+            frame[:, oy:oy + 40, ox:ox + 40] = obj_tex
+        seq.append((np.ascontiguousarray(frame, np.float32), H))
+    return seq
+
+
 def toy_net3(rng=None):
     """netgen.hpp:46-56 shape: conv 3->4 (+b), relu, conv 4->2 (+b), output."""
     rng = rng or np.random.default_rng(43)
