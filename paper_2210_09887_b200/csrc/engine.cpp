@@ -742,6 +742,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     }
 
     // layers in topological order (engine.cpp:247-281)
+    bool densified = false;  // the output layer's activation launch also densified
     for (int idx2 : net_.topo) {
         const Layer& l = net_.layers[idx2];
         LayerRT& rt = lrt_[idx2];
@@ -788,8 +789,18 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                 {
                     // two streaming passes: tile max (+ the halo stash), then fire / fold (kernels_hbm.cu)
                     const int pi = prof_begin(DFX_FAM_TRUNC);
+                    // the output layer densifies inside its activation launch
+                    static const bool fuse_out = !(getenv("DFX_FUSE_OUT") && getenv("DFX_FUSE_OUT")[0] == '0');
+                    DenseOut dz{nullptr, Readback{}};
+                    if (fuse_out && idx2 == net_.out_layer)
+                        dz = DenseOut{out_cur_ ? out_cur_ : out_d_.p,
+                                      Readback{counters_d_.p, (int)(net_.layers.size() * 8 + 8), in_pkt_ext_.p,
+                                               rows_ * cols_, readback_d_, pend_out_flag_, pend_out_val_}};
+                    bool dzd = false;
                     const bool two = launch_trunc_two_pass(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots,
-                                                           rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt, gbars + idx2);
+                                                           rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt, gbars + idx2,
+                                                           dz.out ? &dz : nullptr, &dzd);
+                    if (dzd) densified = true;
                     prof_end(pi);
                     if (two) {
                         launches_ += 1;
@@ -820,7 +831,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     const LayerRT& ort = lrt_[net_.out_layer];
     const Readback rb{counters_d_.p, (int)(net_.layers.size() * 8 + 8), in_pkt_ext_.p, rows_ * cols_, readback_d_,
                       pend_out_flag_, pend_out_val_};
-    PROF(DFX_FAM_DENSIFY, launch_densify(C, s, ort.acc, ort.aux, out_cur_ ? out_cur_ : out_d_.p, rb));
+    if (!densified) PROF(DFX_FAM_DENSIFY, launch_densify(C, s, ort.acc, ort.aux, out_cur_ ? out_cur_ : out_d_.p, rb));
     CUDA_CHECK(cudaGetLastError());
 
     // the small readback (per-layer target counts, dropped, fired input tiles) is

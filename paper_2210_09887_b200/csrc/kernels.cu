@@ -16,6 +16,8 @@ namespace dfx {
 
 namespace {
 
+#include "output.inc.cuh"
+
 constexpr int kThreads = 256;
 
 // TileLedger::holds (buffer_manager.hpp:41-44): placement tiles read the
@@ -550,19 +552,6 @@ __device__ unsigned g_begin_done;
 // after ~4 s instead of hanging the GPU).
 __global__ void k_set_flag(unsigned* f, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
-}
-__device__ __forceinline__ void wait_flag(const unsigned* f, unsigned v) {
-    if (!f) return;
-    if (threadIdx.x == 0) {
-        unsigned x;
-        for (long long it = 0;; ++it) {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(f) : "memory");
-            if ((int)(x - v) >= 0) break;
-            if (it > (1LL << 24)) __trap();
-            __nanosleep(256);
-        }
-    }
-    __syncthreads();
 }
 __global__ void k_frame_begin(const uint4* __restrict__ src, uint4* __restrict__ dst, int n16,
                               uint4* __restrict__ counters, int cnt16, volatile unsigned* ack, unsigned seq,
@@ -1349,58 +1338,11 @@ __global__ void k_add(Ctx c, PktDev a, PktDev b, PktDev out) {
 // Output = acc + trunc over the placement, CHW (delta_layers.cpp:395-400).
 // C % 8 == 0: a warp takes (8-channel group, output row); each lane one pixel:
 // 2 x 16-B reads of acc and trunc, 8 plane writes coalesced across the warp.
-// The frame's small readback (per-layer counts, dropped pixels, fired input
-// tiles) written by CTA 0 of the last kernel straight into mapped host memory.
-__device__ __forceinline__ void frame_readback(const Readback& rb) {
-    if (blockIdx.x != 0 || !rb.dst) return;
-    for (int i = threadIdx.x; i < rb.n1; i += blockDim.x) rb.dst[i] = rb.src1[i];
-    for (int i = threadIdx.x; i < rb.n2; i += blockDim.x) rb.dst[rb.n1 + i] = rb.src2[i];
-}
 __global__ void k_densify8(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ out, int trace, Readback rb) {
     pdl_enter();
     wait_flag(rb.out_flag, rb.out_val);  // host path: the output slot's previous copy-out is done
     frame_readback(rb);
-    const FrameDev& F = *c.f;
-    const int t = acc.t, C = acc.C, G = C / 8;
-    const int oh = F.th * t, ow = F.tw * t;
-    const size_t plane = (size_t)oh * ow;
-    const int lane = threadIdx.x & 31;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-    for (int it = gw; it < G * oh; it += nw) {
-        const int g = it / oh, y = it - g * oh;
-        const int qy = y / t, yy = y - qy * t;
-        // two pixels per lane per round, all 8 loads issued before any use
-        for (int x0 = lane; x0 < ow; x0 += 64) {
-            float4 a0[2], a1[2], t0[2], t1[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int x = x0 + 32 * u;
-                if (x < ow) {
-                    const int qx = x / t;
-                    const size_t off = (size_t)slot_of(F, c.rows, c.cols, qy, qx) * t * t * C +
-                                       ((size_t)yy * t + (x - qx * t)) * C + g * 8;
-                    a0[u] = __ldcs(reinterpret_cast<const float4*>(acc.d + off));
-                    a1[u] = __ldcs(reinterpret_cast<const float4*>(acc.d + off) + 1);
-                    t0[u] = __ldcs(reinterpret_cast<const float4*>(trunc.d + off));
-                    t1[u] = __ldcs(reinterpret_cast<const float4*>(trunc.d + off) + 1);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int x = x0 + 32 * u;
-                if (x >= ow) continue;
-                float* o = out + (size_t)(g * 8) * plane + (size_t)y * ow + x;
-                o[0] = __fadd_rn(a0[u].x, t0[u].x);
-                o[plane] = __fadd_rn(a0[u].y, t0[u].y);
-                o[2 * plane] = __fadd_rn(a0[u].z, t0[u].z);
-                o[3 * plane] = __fadd_rn(a0[u].w, t0[u].w);
-                o[4 * plane] = __fadd_rn(a1[u].x, t1[u].x);
-                o[5 * plane] = __fadd_rn(a1[u].y, t1[u].y);
-                o[6 * plane] = __fadd_rn(a1[u].z, t1[u].z);
-                o[7 * plane] = __fadd_rn(a1[u].w, t1[u].w);
-            }
-        }
-    }
+    densify8_body(c, acc, trunc, out, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5);
     if (trace) {
         __syncthreads();
         if (threadIdx.x == 0) {

@@ -51,8 +51,25 @@ bool launch_trunc_fused(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, Buf
                         PktDev out);
 // Two streaming passes (kernels_hbm.cu): tile max, then fire / fold. Needs C % 4 == 0.
 // gbar (zeroed per frame): grid-barrier counter for the single cooperative launch.
+struct Readback {  // copied by the last kernel of a frame into mapped host memory
+    const uint8_t* src1;
+    int n1;
+    const uint8_t* src2;
+    int n2;
+    uint8_t* dst;  // device view of the page-locked host block
+    const unsigned* out_flag = nullptr;  // host path: wait until *out_flag >= out_val before writing the output
+    unsigned out_val = 0;
+};
+
+// Output layer: densify (acc + trunc -> the frame's output, plus the frame's
+// readback) inside the cooperative activation launch (dz_done reports it).
+struct DenseOut {
+    float* out;
+    Readback rb;
+};
 bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
-                           float thr, int relu, PktDev out, unsigned* gbar);
+                           float thr, int relu, PktDev out, unsigned* gbar, const DenseOut* dz = nullptr,
+                           bool* dz_done = nullptr);
 bool launch_maxpool_vec(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, PktDev out);
 void launch_trunc_apply(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
                         const unsigned* tile_max, float thr, int relu, PktDev out);
@@ -126,15 +143,6 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
                        int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms);
 
 // ---- output (delta_layers.cpp:395-400) ----
-struct Readback {  // copied by the last kernel of a frame into mapped host memory
-    const uint8_t* src1;
-    int n1;
-    const uint8_t* src2;
-    int n2;
-    uint8_t* dst;  // device view of the page-locked host block
-    const unsigned* out_flag = nullptr;  // host path: wait until *out_flag >= out_val before writing the output
-    unsigned out_val = 0;
-};
 void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out, Readback rb);
 // Fused input stage (no ROI factor, no noise filter): A = align + coverage +
 // significance per canvas tile, B = gate + input truncation per tile.

@@ -25,6 +25,8 @@ namespace dfx {
 
 namespace {
 
+#include "output.inc.cuh"
+
 #ifndef DFX_TRUNC_MINB  // CTAs per SM of k_trunc_coop (measured: 3 -> 80 registers with spills, slower)
 #define DFX_TRUNC_MINB 2
 #endif
@@ -376,7 +378,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr) {
 
 __global__ void __launch_bounds__(256, DFX_TRUNC_MINB) k_trunc_coop(Ctx c, PktDev in, BufDev acc, BufDev trunc,
                                                     unsigned* __restrict__ tile_max, float thr, int relu, PktDev out,
-                                                    unsigned* __restrict__ gbar, unsigned long long* tr, int dry) {
+                                                    unsigned* __restrict__ gbar, unsigned long long* tr, int dry,
+                                                    DenseOut dz) {
     tstamp(tr, 0);
     // touch every kernel parameter up front: their constant-bank lines miss once, together
     asm volatile("" ::"l"(in.d), "l"(in.ext), "r"(in.C), "r"(in.t), "r"(in.halo), "r"(in.RT), "r"(in.pitch_w),
@@ -411,6 +414,26 @@ __global__ void __launch_bounds__(256, DFX_TRUNC_MINB) k_trunc_coop(Ctx c, PktDe
     __syncthreads();
     tstamp(tr, 5);
     commit_body(c, F, in, acc, trunc, tile_max, thr, relu, out, s_list, nl, true);
+    if (dz.out) {
+        // output layer: densify acc + trunc into the frame's output after a
+        // second grid barrier (same counter), saving the densify launch
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gbar) : "memory");
+            unsigned v;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gbar) : "memory");
+                if (v >= 2 * gridDim.x) break;
+                __nanosleep(32);
+            }
+        }
+        __syncthreads();
+        wait_flag(dz.rb.out_flag, dz.rb.out_val);  // host path: the output slot's previous copy-out is done
+        frame_readback(dz.rb);
+        densify8_body(c, acc, trunc, dz.out, (blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+                      (gridDim.x * blockDim.x) >> 5);
+    }
     __syncthreads();
     tstamp(tr, 6);
 }
@@ -496,7 +519,9 @@ static unsigned long long* g_trunc_trace = nullptr;
 unsigned long long* trunc_trace_buffer() { return g_trunc_trace; }
 
 bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
-                           float thr, int relu, PktDev out, unsigned* gbar) {
+                           float thr, int relu, PktDev out, unsigned* gbar, const DenseOut* dzp, bool* dz_done) {
+    if (dz_done) *dz_done = false;
+    const DenseOut dz = (dzp && (acc.C & 7) == 0) ? *dzp : DenseOut{nullptr, Readback{}};
     if ((in.C & 3) != 0) return false;
     static const int gc = stream_grid(k_trunc_coop);
     static const bool coop_ok = [] {
@@ -513,7 +538,7 @@ bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, 
     g_trunc_trace = trace;
     static const bool warm = getenv("DFX_TRUNC_WARM") != nullptr;  // experiment
     if (warm) launch_pdl(k_trunc_coop, gc, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out, gbar,
-                         (unsigned long long*)nullptr, 1);
+                         (unsigned long long*)nullptr, 1, DenseOut{nullptr, Readback{}});
     if (gbar && coop_ok) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(gc);
@@ -526,8 +551,11 @@ bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, 
         attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = pdl_enabled() ? 2 : 1;
-        if (cudaLaunchKernelEx(&cfg, k_trunc_coop, c, in, acc, trunc, tile_max, thr, relu, out, gbar, tr, 0) == cudaSuccess)
+        if (cudaLaunchKernelEx(&cfg, k_trunc_coop, c, in, acc, trunc, tile_max, thr, relu, out, gbar, tr, 0, dz) ==
+            cudaSuccess) {
+            if (dz_done) *dz_done = dz.out != nullptr;
             return true;
+        }
         cudaGetLastError();  // fall back to two launches
     }
     static const int g1 = stream_grid(k_trunc_tilemax), g2 = stream_grid(k_trunc_commit);
