@@ -30,6 +30,6 @@ d = np.diff(t) / 1e3
 print(f"{n} stamps, {per} kernels per frame; frame period {np.median(np.diff(t[::per])) / 1e3:.1f} us")
 last = d[-per + 1:]
 names = os.environ.get("KNAMES", "").split(",")
-for i, v in enumerate(last):
-    print(f"{i + 1:3d} {v:7.1f} us  {names[i + 1] if i + 1 < len(names) else ''}")
-print(f"sum {last.sum():.1f} us (kernel 0 of the frame excluded)")
+for i, v in enumerate(last):  # index 0 = the frame's first kernel (k_frame_begin)
+    print(f"{i:3d} {v:7.1f} us  {names[i] if i < len(names) else ''}")
+print(f"sum {last.sum():.1f} us (the frame's last kernel excluded)")
