@@ -703,7 +703,8 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     const int nslots = rows_ * cols_;
 
     // claims reset + implicit bias (buffer_manager.cpp:68-89)
-    PROF(DFX_FAM_CLAIMS, launch_claims(C, s, d_claims_, claim_bufs_.p, nclaim_bufs_, max_claims_));
+    // (the host knows the claim count: frames without claims skip the launch)
+    if (F.nclaims > 0) PROF(DFX_FAM_CLAIMS, launch_claims(C, s, d_claims_, claim_bufs_.p, nclaim_bufs_, max_claims_));
 
     // input stage
     static const bool fuse_input = !(getenv("DFX_FUSE_INPUT") && getenv("DFX_FUSE_INPUT")[0] == '0');
