@@ -2,7 +2,7 @@
 set -x
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -3 gpurun_out/smoke.log
 timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -3
-timeout 600 python bench.py --steps 20 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err  # the driver's default command
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/ncu_probe.py 10 > gpurun_out/ncu_probe.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_conv_dense|k_conv_tc|k_conv_plan" -s 60 -c 12 -o gpurun_out/conv_full python tools/ncu_probe.py 6 > gpurun_out/ncu_conv.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_trunc|k_maxpool|k_claims|k_input|k_densify" -s 80 -c 30 -o gpurun_out/hbm_full python tools/ncu_probe.py 6 > gpurun_out/ncu_hbm.log 2>&1
