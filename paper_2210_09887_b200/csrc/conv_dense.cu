@@ -834,10 +834,6 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     if (const char* u = getenv("DFX_DENSE_UMAX")) p.umax = (atoi(u) >= 2 && p.cin_pad % 16 == 0) ? 2 : 1;
     // 16-channel K-blocks: 16 KB weight stages, a deeper ring hides the bulk-copy latency (measured +2-4%)
     p.KC = p.cin_pad % 16 == 0 ? 16 : 8;
-    if (const char* kc = getenv("DFX_DENSE_KC")) {  // experiments: 32-channel K-blocks
-        const int v = atoi(kc);
-        if ((v == 16 || v == 32) && p.cin_pad % v == 0) p.KC = v;
-    }
     p.r = k / 2;
     p.k = k;
     // Tile units (T = t_out in {2, 4, 8}): a unit is 128 / T^2 ACTIVE output
