@@ -477,6 +477,37 @@ __global__ void __launch_bounds__(256) k_maxpool_vec(Ctx c, PktDev in, BufDev ac
                 *d = make_float4(0.f, 0.f, 0.f, 0.f);
                 continue;
             }
+            if (k == 2) {
+                // 2x2 window: all nine loads (4 acc, 4 delta, prev) in flight before any use
+                float4* ap[4];
+                float4 av[4], dv[4];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    const int iy = y * 2 + (w >> 1), ix = x * 2 + (w & 1);
+                    ap[w] = ab + ((size_t)iy * ti_ + ix) * C4 + c4;
+                    av[w] = __ldcs(ap[w]);
+                    dv[w] = __ldcg(reinterpret_cast<const float4*>(in.d + pkt_off(in, tr * ti_ + iy, tc * ti_ + ix)) + c4);
+                }
+                float4* pp = pb + ((size_t)y * to + x) * C4 + c4;
+                const float4 pv = __ldcs(pp);
+                float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    const float4 v = add4(av[w], dv[w]);
+                    __stcs(ap[w], v);
+                    if (w == 0) {
+                        m = v;
+                    } else {  // std::max(m, v) == (m < v) ? v : m
+                        m.x = m.x < v.x ? v.x : m.x;
+                        m.y = m.y < v.y ? v.y : m.y;
+                        m.z = m.z < v.z ? v.z : m.z;
+                        m.w = m.w < v.w ? v.w : m.w;
+                    }
+                }
+                *d = make_float4(__fsub_rn(m.x, pv.x), __fsub_rn(m.y, pv.y), __fsub_rn(m.z, pv.z), __fsub_rn(m.w, pv.w));
+                __stcs(pp, m);
+                continue;
+            }
             float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int ky = 0; ky < k; ++ky)
                 for (int kx = 0; kx < k; ++kx) {
