@@ -152,6 +152,7 @@ struct DenseArgs {
     int ppx;               // pixels of one unit's patch
     int npb;               // patch ring depth (raw fp32 patches; the producers split hi / lo)
     int nmma;              // MMA issuer warps (2: K-block pairs alternate, one accumulator each)
+    BufDev nxt_acc, nxt_trunc;  // the consuming activation's state (L2 prefetch of this CTA's tiles), .d = null: none
     long long* trace;      // microbenchmark (dbg & 64): per-K-block clock64 stamps of CTA 0
     int dbg;               // microbenchmark knobs (tools/bench_conv.cu): 1 no MMA, 2 no patch, 4 no weights
 };
@@ -532,6 +533,22 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
             int pr, nb, kb0, kb1;
             item_info(it, pr, nb, kb0, kb1);
             const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
+            // while this item's MMAs run: tile units start the consuming activation's acc / trunc tiles of this
+            // item towards L2 (its first, latency-bound pass reads them right after)
+            if (a.tpu && a.nxt_acc.d && m < 2 * a.tpu) {
+                const int s = m >> 1, li = pr * a.tpu + s;
+                if (li < listed) {
+                    const int tv = __ldcg(a.units + li);
+                    const int tr = (tv >> 16) - 8, tc = (tv & 0xffff) - 8;
+                    const BufDev& bd = (m & 1) ? a.nxt_trunc : a.nxt_acc;
+                    const uint32_t bytes = (uint32_t)bd.t * bd.t * bd.C * 4;
+                    if (tr >= 0 && tr < F.th && tc >= 0 && tc < F.tw && (bytes & 15) == 0)
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                         bd.d + (size_t)slot_of(F, c.rows, c.cols, tr, tc) * bd.t * bd.t * bd.C),
+                                     "r"(bytes)
+                                     : "memory");
+                }
+            }
             const uint32_t b = a.nbuf == 2 ? (ui & 1) : 0, ub = a.nbuf == 2 ? (ui >> 1) : ui;
             mbar_wait(smem_u32(&bar_af[b]), ub & 1);
             const long long t_e0 = clock64();
@@ -974,12 +991,13 @@ static void launch_kc(int grid, size_t smem, cudaStream_t s, const Ctx& c, const
 static long long* g_trace = nullptr;
 long long* dense_conv_trace_buffer() { return g_trace; }
 void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,
-                       int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms) {
+                       int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms,
+                       BufDev nxt_acc, BufDev nxt_trunc) {
     if (!p.ok) throw std::runtime_error("conv_dense: unsupported layer shape");
     DenseArgs a{in, out, w, units, nunits, p.smax > 1 ? ws : nullptr, cnt, cin, cout, p.cout_pad, p.k, p.r,
                 p.KC, p.nCB, p.NBD, p.nNB, p.nstw, p.smax > 1 ? p.smax : 1, num_sms, p.s_c4, p.patch_bytes,
                 p.w_stage, p.acc_cols, p.nbuf, p.nbuf * p.acc_cols, p.umax, p.tpu, p.tsh, p.patch_px, p.npb,
-                p.nmma, nullptr, 0};
+                p.nmma, nxt_acc, nxt_trunc, nullptr, 0};
     if (getenv("DFX_CONV_DBG") && !g_trace) cudaMalloc(&g_trace, 2048 * 8);
     a.trace = g_trace;
     if (const char* d = getenv("DFX_CONV_DBG")) a.dbg = atoi(d);

@@ -767,8 +767,19 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                                                               l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom, rt.list.p,
                                                               counts + idx2, rt.max_targets, num_sms_, rt.ws.p,
                                                               rt.splits));
-                    PROF(DFX_FAM_CONV_MMA, launch_conv_dense(C, s, rt.dp, a, rt.pkt, rt.wdense.p, l.cin, l.cout,
-                                                             rt.units.p, ucounts + idx2, rt.wsd.p, rt.dcnt.p, num_sms_));
+                    {
+                        // the sole consuming activation's state: prefetched to L2 by the conv
+                        BufDev na{nullptr, 0, 0}, nt{nullptr, 0, 0};
+                        int cj = -1, ncons = 0;
+                        for (size_t j = 0; j < net_.layers.size(); ++j)
+                            if (net_.layers[j].in0 == idx2 || net_.layers[j].in1 == idx2) cj = (int)j, ++ncons;
+                        if (ncons == 1 && (net_.layers[cj].kind == DFX_RELU || net_.layers[cj].kind == DFX_TRUNCATE ||
+                                           net_.layers[cj].kind == DFX_OUTPUT))
+                            na = lrt_[cj].acc, nt = lrt_[cj].aux;
+                        PROF(DFX_FAM_CONV_MMA, launch_conv_dense(C, s, rt.dp, a, rt.pkt, rt.wdense.p, l.cin, l.cout,
+                                                                 rt.units.p, ucounts + idx2, rt.wsd.p, rt.dcnt.p,
+                                                                 num_sms_, na, nt));
+                    }
                     break;
                 }
                 PROF(DFX_FAM_CONV_TARGETS, launch_conv_targets(C, s, a, l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom, rt.list.p, counts + idx2,

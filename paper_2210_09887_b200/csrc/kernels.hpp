@@ -139,8 +139,11 @@ void ktrace_set_dense(unsigned long long* b, unsigned* c);
 void ktrace_set_tc(unsigned long long* b, unsigned* c);
 unsigned long long* frame_trace_host();  // DFX_FRAME_TRACE: [64][4] frame-boundary stamps
 unsigned long long* trunc_trace_buffer();  // DFX_TRUNC_TRACE: [64 launches][1024 CTAs][8] globaltimer stamps  // microbenchmark stamps (DFX_CONV_DBG & 64)
+// nxt_acc / nxt_trunc: the consuming activation layer's state buffers (its tiles
+// are prefetched to L2 by the conv), or {nullptr} for none.
 void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,
-                       int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms);
+                       int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms,
+                       BufDev nxt_acc = BufDev{nullptr, 0, 0}, BufDev nxt_trunc = BufDev{nullptr, 0, 0});
 
 // ---- output (delta_layers.cpp:395-400) ----
 void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out, Readback rb);
