@@ -535,11 +535,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
             const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
             // while this item's MMAs run: tile units start the consuming activation's acc / trunc tiles of this
             // item towards L2 (its first, latency-bound pass reads them right after)
-            if (a.tpu && a.nxt_acc.d && m < 2 * a.tpu) {
-                const int s = m >> 1, li = pr * a.tpu + s;
-                if (li < listed) {
+            // (16x8 units: the one 16-px-or-larger output tile the unit lies in)
+            if (a.nxt_acc.d && m < 2 * (a.tpu ? a.tpu : UPI)) {
+                const int s = m >> 1, li = a.tpu ? pr * a.tpu + s : UPI * pr + s;
+                if (li < (a.tpu ? listed : n)) {
                     const int tv = __ldcg(a.units + li);
-                    const int tr = (tv >> 16) - 8, tc = (tv & 0xffff) - 8;
+                    const int T = a.out.t;
+                    const int tr = a.tpu ? (tv >> 16) - 8 : floor_div32(((tv >> 16) - 1) * kUY, T);
+                    const int tc = a.tpu ? (tv & 0xffff) - 8 : floor_div32(((tv & 0xffff) - 1) * kUX, T);
                     const BufDev& bd = (m & 1) ? a.nxt_trunc : a.nxt_acc;
                     const uint32_t bytes = (uint32_t)bd.t * bd.t * bd.C * 4;
                     if (tr >= 0 && tr < F.th && tc >= 0 && tc < F.tw && (bytes & 15) == 0)
