@@ -812,9 +812,17 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                                       Readback{counters_d_.p, (int)(net_.layers.size() * 8 + 8), in_pkt_ext_.p,
                                                rows_ * cols_, readback_d_, pend_out_flag_, pend_out_val_}};
                     bool dzd = false;
+                    // a sole consuming max pool: its acc / prev tiles of every fired tile go to L2
+                    BufDev pf0{nullptr, 0, 0}, pf1{nullptr, 0, 0};
+                    {
+                        int pj = -1, ncons = 0;
+                        for (size_t j = 0; j < net_.layers.size(); ++j)
+                            if (net_.layers[j].in0 == idx2 || net_.layers[j].in1 == idx2) pj = (int)j, ++ncons;
+                        if (ncons == 1 && net_.layers[pj].kind == DFX_MAXPOOL) pf0 = lrt_[pj].acc, pf1 = lrt_[pj].aux;
+                    }
                     const bool two = launch_trunc_two_pass(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots,
                                                            rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt, gbars + idx2,
-                                                           dz.out ? &dz : nullptr, &dzd);
+                                                           dz.out ? &dz : nullptr, &dzd, pf0, pf1);
                     if (dzd) densified = true;
                     prof_end(pi);
                     if (two) {

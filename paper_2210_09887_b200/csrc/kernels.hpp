@@ -69,7 +69,8 @@ struct DenseOut {
 };
 bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
                            float thr, int relu, PktDev out, unsigned* gbar, const DenseOut* dz = nullptr,
-                           bool* dz_done = nullptr);
+                           bool* dz_done = nullptr, BufDev pf0 = BufDev{nullptr, 0, 0},
+                           BufDev pf1 = BufDev{nullptr, 0, 0});  // pf0 / pf1: consumer state prefetched per fired tile
 bool launch_maxpool_vec(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, PktDev out);
 void launch_trunc_apply(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
                         const unsigned* tile_max, float thr, int relu, PktDev out);

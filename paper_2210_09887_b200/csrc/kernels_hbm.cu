@@ -279,7 +279,8 @@ __global__ void __launch_bounds__(256) k_trunc_tilemax(Ctx c, PktDev in, BufDev 
 // Pass 2: output mask of every placement tile, then fire / fold of the masked ones.
 __device__ void commit_body(const Ctx& c, const FrameDev& F, const PktDev& in, BufDev acc, BufDev trunc,
                             const unsigned* __restrict__ tile_max, float thr, int relu, const PktDev& out,
-                            const int* s_list, int nl, bool ext_by_items = false) {
+                            const int* s_list, int nl, bool ext_by_items = false,
+                            const BufDev* pf0 = nullptr, const BufDev* pf1 = nullptr) {
     const int T = in.t, E4 = T * T * in.C / 4;
     const Div row4(T * in.C / 4), nch((E4 + kChunkF4 - 1) / kChunkF4);
     // output mask = fired tiles (delta_layers.cpp:203-204), every placement tile
@@ -300,7 +301,19 @@ __device__ void commit_body(const Ctx& c, const FrameDev& F, const PktDev& in, B
         if (nl < 0 && (!in.ext[ext_idx(in, tr, tc)] || !holds_t(c, F, tr, tc))) continue;
         const float tm = __uint_as_float(__ldcg(tile_max + ti));
         const bool fire = tm >= thr && tm > 0.0f;
-        if (ext_by_items && nl >= 0 && ch == 0 && lane == 0) out.ext[ext_idx(out, tr, tc)] = fire ? 1 : 0;
+        if (ext_by_items && nl >= 0 && ch == 0 && lane == 0) {
+            out.ext[ext_idx(out, tr, tc)] = fire ? 1 : 0;
+            if (fire && pf0) {  // the consuming pool's state tiles of this fired tile, towards L2
+                const int sl = slot_of(F, c.rows, c.cols, tr, tc);
+                const uint32_t b0 = (uint32_t)pf0->t * pf0->t * pf0->C * 4, b1 = (uint32_t)pf1->t * pf1->t * pf1->C * 4;
+                if ((b0 & 15) == 0)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf0->d + (size_t)sl * b0 / 4), "r"(b0)
+                                 : "memory");
+                if ((b1 & 15) == 0)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf1->d + (size_t)sl * b1 / 4), "r"(b1)
+                                 : "memory");
+            }
+        }
         float4* tb = reinterpret_cast<float4*>(tile_base(c, F, trunc, tr, tc));
         float4* ab = reinterpret_cast<float4*>(tile_base(c, F, acc, tr, tc));
         const int q0 = ch * kChunkF4, q1 = min(E4, q0 + kChunkF4);
@@ -379,7 +392,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr) {
 __global__ void __launch_bounds__(256, DFX_TRUNC_MINB) k_trunc_coop(Ctx c, PktDev in, BufDev acc, BufDev trunc,
                                                     unsigned* __restrict__ tile_max, float thr, int relu, PktDev out,
                                                     unsigned* __restrict__ gbar, unsigned long long* tr, int dry,
-                                                    DenseOut dz) {
+                                                    DenseOut dz, BufDev pf0, BufDev pf1) {
     tstamp(tr, 0);
     // touch every kernel parameter up front: their constant-bank lines miss once, together
     asm volatile("" ::"l"(in.d), "l"(in.ext), "r"(in.C), "r"(in.t), "r"(in.halo), "r"(in.RT), "r"(in.pitch_w),
@@ -413,7 +426,8 @@ __global__ void __launch_bounds__(256, DFX_TRUNC_MINB) k_trunc_coop(Ctx c, PktDe
     }
     __syncthreads();
     tstamp(tr, 5);
-    commit_body(c, F, in, acc, trunc, tile_max, thr, relu, out, s_list, nl, true);
+    commit_body(c, F, in, acc, trunc, tile_max, thr, relu, out, s_list, nl, true, pf0.d ? &pf0 : nullptr,
+                pf1.d ? &pf1 : nullptr);
     if (dz.out) {
         // output layer: densify acc + trunc into the frame's output after a
         // second grid barrier (same counter), saving the densify launch
@@ -550,7 +564,8 @@ static unsigned long long* g_trunc_trace = nullptr;
 unsigned long long* trunc_trace_buffer() { return g_trunc_trace; }
 
 bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
-                           float thr, int relu, PktDev out, unsigned* gbar, const DenseOut* dzp, bool* dz_done) {
+                           float thr, int relu, PktDev out, unsigned* gbar, const DenseOut* dzp, bool* dz_done,
+                           BufDev pf0, BufDev pf1) {
     if (dz_done) *dz_done = false;
     const DenseOut dz = (dzp && (acc.C & 7) == 0) ? *dzp : DenseOut{nullptr, Readback{}};
     if ((in.C & 3) != 0) return false;
@@ -569,7 +584,8 @@ bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, 
     g_trunc_trace = trace;
     static const bool warm = getenv("DFX_TRUNC_WARM") != nullptr;  // experiment
     if (warm) launch_pdl(k_trunc_coop, gc, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out, gbar,
-                         (unsigned long long*)nullptr, 1, DenseOut{nullptr, Readback{}});
+                         (unsigned long long*)nullptr, 1, DenseOut{nullptr, Readback{}}, BufDev{nullptr, 0, 0},
+                         BufDev{nullptr, 0, 0});
     if (gbar && coop_ok) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(gc);
@@ -582,7 +598,7 @@ bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, 
         attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = pdl_enabled() ? 2 : 1;
-        if (cudaLaunchKernelEx(&cfg, k_trunc_coop, c, in, acc, trunc, tile_max, thr, relu, out, gbar, tr, 0, dz) ==
+        if (cudaLaunchKernelEx(&cfg, k_trunc_coop, c, in, acc, trunc, tile_max, thr, relu, out, gbar, tr, 0, dz, pf0, pf1) ==
             cudaSuccess) {
             if (dz_done) *dz_done = dz.out != nullptr;
             return true;
