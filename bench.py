@@ -390,7 +390,7 @@ def run_ours(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             try:
-                cb = cpu_reference(steps=2, warmup=1, full_gflop=conv_gflop)
+                cb = cpu_reference(steps=8, warmup=1, full_gflop=conv_gflop)  # ~10 s of host work
                 line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
             except Exception as e:  # the baseline is reported, not the target
                 line["cpu_baseline"] = {"value": None, "unit": "frames/s", "cores": 0, "kind": "reference",
