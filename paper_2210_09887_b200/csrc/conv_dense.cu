@@ -418,10 +418,22 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     // Prologue: the CTA's first patch (offsets + first channel chunk) is built by
     // ALL threads, so the first MMA is not gated by 4 loader warps walking a
     // dependent chain alone (~4-6 us per launch before).
+    int w_pre = 0;  // weight stages of the first item already requested (weight-producer lane only)
     {
         int pr, nb, kb0, kb1;
         item_info(blockIdx.x, pr, nb, kb0, kb1);
         const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
+        if (warp == 4 * kProdWG + 9 && lane == 0 && !(a.dbg & 4)) {
+            // the first stages' weights are requested before the patch is built (the
+            // stages are free at kernel start): they land while the prologue runs
+            const float* wnb = a.w + (size_t)nb * nKB * (a.w_stage / 4);
+            w_pre = min(NST, kb1 - kb0);
+            for (int i = 0; i < w_pre; ++i) {
+                mbar_arrive_tx(smem_u32(&bar_full[i]), a.w_stage);
+                bulk_g2s(w_base + i * a.w_stage, wnb + (size_t)(kb0 + i) * (a.w_stage / 4), a.w_stage,
+                         smem_u32(&bar_full[i]));
+            }
+        }
         patch_offsets(pr, nu, tid, kDenseThreads);
         __syncthreads();
         copy_chunk(sbase, (kb0 / K2) * KC, nu, tid, kDenseThreads);
@@ -709,6 +721,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                 int pr, nb, kb0, kb1;
                 item_info(it, pr, nb, kb0, kb1);
                 const float* wnb = a.w + (size_t)nb * nKB * (a.w_stage / 4);
+                if (it == (int)blockIdx.x && w_pre > 0) {  // skip the stages the prologue requested
+                    kb0 += w_pre;
+                    st = (uint32_t)(w_pre % NST);
+                    ph = w_pre == NST ? 1u : 0u;
+                }
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(smem_u32(&bar_empty[st]), ph ^ 1);
                     if (a.dbg & 4) {
