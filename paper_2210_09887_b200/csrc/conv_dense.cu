@@ -620,12 +620,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                     s_last = atomicAdd(a.cnt + it / S, 1) == S - 1;
                 }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
-                // every split CTA reduces 1/S of the tile's rows at the end of the
-                // kernel with ALL its threads once the S partials are in (S > 1
-                // implies one item per CTA, all CTAs resident: the wait cannot
-                // deadlock); 128 epilogue threads of one CTA made it a chain of
-                // dependent L2 round trips at the layer's tail
-                if (q == 0 && lane == 0) s_red_it = it;
+                // the CTA whose partial arrives last sums all S partials at the end
+                // of the kernel with ALL its threads (no CTA ever waits for another:
+                // safe with several engines sharing the GPU, where not every CTA of
+                // a grid need be resident at once)
+                if (s_last && q == 0 && lane == 0) s_red_it = it;
             }
             if ((a.dbg & 64) && blockIdx.x == 0 && tid == 128 * kProdWG + 128 && ui < 4) {
                 a.trace[504 + 2 * ui] = t_e0;
@@ -747,22 +746,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
     tc_fence_after();
     if (s_red_it >= 0) {
         // fixed-order (split 0, 1, ...) sum of the S partials of one (unit group,
-        // N-block) tile into the packet: this split CTA takes rows [ks*128/S,
-        // (ks+1)*128/S), every thread float4 columns of those rows, all S loads of
-        // a float4 in flight before the adds (deterministic order)
+        // N-block) tile into the packet: every thread float4 columns of rows, all
+        // S loads of a float4 in flight before the adds (deterministic order)
         const int it = s_red_it;
-        if (tid == 0) {
-            unsigned v;
-            for (long long spin = 0;; ++spin) {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.cnt + it / S) : "memory");
-                if ((int)v >= S) break;
-                if (spin > (1LL << 26)) __trap();
-                __nanosleep(64);
-            }
-        }
-        __syncthreads();
         __threadfence();
-        const int ks = it % S, m0 = 128 * ks / S, m1 = 128 * (ks + 1) / S, nm = m1 - m0;
+        const int m0 = 0, nm = 128;
         int pr, nb, kb0, kb1;
         item_info(it, pr, nb, kb0, kb1);
         const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
@@ -800,10 +788,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                 for (int q = 0; q < 4 && o + q < o1; ++q) dst[q] = vv[q];
             }
         }
-        __syncthreads();
-        if (tid == 0) {  // second round of arrivals: the last reducer re-arms the counter
-            if (atomicAdd(a.cnt + it / S, 1) == 2 * S - 1) a.cnt[it / S] = 0;
-        }
+        if (tid == 0) a.cnt[it / S] = 0;  // re-arm for the next frame
     }
     if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) a.trace[501] = clock64();
     if ((a.dbg & 64) && tid == 0 && blockIdx.x < 400) {

@@ -238,6 +238,7 @@ class Engine {
     unsigned* ack_d_ = nullptr;
     unsigned fseq_ = 0, pslot_seq_[2] = {0, 0};
     uint8_t* readback_d_ = nullptr;                // device view of readback_h_
+    DevArr<unsigned> begin_ctr_;                   // k_frame_begin's last-CTA counter (per engine)
     // host path: copy-stream -> engine-stream flags [h2d slot 0, 1, d2h slot 0, 1]
     DevArr<unsigned> hflags_;
     const unsigned* pend_in_flag_ = nullptr;
@@ -526,6 +527,8 @@ void Engine::allocate(int th, int tw) {
     CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&ack_h_), 64, cudaHostAllocMapped));
     *reinterpret_cast<volatile unsigned*>(ack_h_) = 0;
     CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ack_d_), ack_h_, 0));
+    begin_ctr_.alloc(1);
+    CUDA_CHECK(cudaMemset(begin_ctr_.p, 0, sizeof(unsigned)));
     fseq_ = 0;
     pslot_seq_[0] = pslot_seq_[1] = 0;
     set_param_slot(0);
@@ -690,7 +693,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     std::atomic_thread_fence(std::memory_order_release);
     launches_ = 0;
     launch_frame_begin(stream_, params_hd_[pslot_], params_d_.p + (size_t)pslot_ * pstride_, pstride_, counters_d_.p,
-                       cnt_bytes_, ack_d_, fseq_, pend_in_flag_, pend_in_val_);
+                       cnt_bytes_, ack_d_, fseq_, pend_in_flag_, pend_in_val_, begin_ctr_.p);
     ++launches_;
     const Ctx C = ctx();
     cudaStream_t s = stream_;

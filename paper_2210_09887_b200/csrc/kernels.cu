@@ -545,7 +545,6 @@ __global__ void k_input_tile_b(Ctx c, const float* __restrict__ aligned, const u
 // programmatic dependent launch end to end. The parameter slot alternates per
 // frame: the copy runs BEFORE the dependency wait, overlapping the previous
 // frame's last kernel, which reads the other slot.
-__device__ unsigned g_begin_done;
 // Cross-stream handshake without stream events (which would cut the engine
 // stream's programmatic-launch chain): a copy stream publishes "copy n done"
 // with k_set_flag, the engine kernel that depends on it polls (bounded: traps
@@ -555,7 +554,7 @@ __global__ void k_set_flag(unsigned* f, unsigned v) {
 }
 __global__ void k_frame_begin(const uint4* __restrict__ src, uint4* __restrict__ dst, int n16,
                               uint4* __restrict__ counters, int cnt16, volatile unsigned* ack, unsigned seq,
-                              const unsigned* in_flag, unsigned in_val) {
+                              const unsigned* in_flag, unsigned in_val, unsigned* done_ctr) {
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     for (int i = tid; i < n16; i += nth) dst[i] = src[i];
     wait_flag(in_flag, in_val);  // host path: this frame's input copy has landed
@@ -564,8 +563,9 @@ __global__ void k_frame_begin(const uint4* __restrict__ src, uint4* __restrict__
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        if (atomicAdd(&g_begin_done, 1u) == gridDim.x - 1) {  // every CTA has read its part of the host block
-            g_begin_done = 0;
+        // per-engine counter (engines sharing a GPU run frame_begin concurrently)
+        if (atomicAdd(done_ctr, 1u) == gridDim.x - 1) {  // every CTA has read its part of the host block
+            *done_ctr = 0;
             *ack = seq;  // the host only needs to see it eventually (it spins); every read above has returned
         }
     }
@@ -1539,12 +1539,30 @@ void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, floa
                out, rb);
 }
 void launch_frame_begin(cudaStream_t s, const void* src, void* dst, size_t bytes, void* counters, size_t cnt_bytes,
-                        unsigned* ack, unsigned seq, const unsigned* in_flag, unsigned in_val) {
+                        unsigned* ack, unsigned seq, const unsigned* in_flag, unsigned in_val, unsigned* done_ctr) {
     launch_pdl(k_frame_begin, 32, kThreads, 0, s, reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst),
                (int)(bytes / 16), reinterpret_cast<uint4*>(counters), (int)(cnt_bytes / 16), (volatile unsigned*)ack,
-               seq, in_flag, in_val);
+               seq, in_flag, in_val, done_ctr);
 }
-void launch_set_flag(cudaStream_t s, unsigned* f, unsigned v) { k_set_flag<<<1, 1, 0, s>>>(f, v); }
+// The flag write is a stream memory operation (cuStreamWriteValue32, executed
+// by the stream front end after the stream's prior work, with a memory barrier):
+// it needs no SM, so a kernel polling the flag can never starve it of one (with
+// several engines on a GPU a flag *kernel* could wait behind polling CTAs).
+// Falls back to a one-thread kernel if the driver entry point is unavailable.
+void launch_set_flag(cudaStream_t s, unsigned* f, unsigned v) {
+    typedef int (*WriteValue32)(cudaStream_t, unsigned long long, unsigned, unsigned);
+    static WriteValue32 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        cudaGetLastError();
+        return reinterpret_cast<WriteValue32>(p);
+    }();
+    if (fn && fn(s, (unsigned long long)(uintptr_t)f, v, 0) == 0) return;
+    k_set_flag<<<1, 1, 0, s>>>(f, v);
+}
 
 DFX_KTRACE_SETTER(ktrace_set_kernels)
 

@@ -156,8 +156,9 @@ void launch_input_tile_a(const Ctx& c, cudaStream_t s, const float* frame, const
 void launch_input_tile_b(const Ctx& c, cudaStream_t s, const float* aligned, const uint8_t* cov, const uint8_t* sig,
                          const uint8_t* fresh, int dilation, int pitch, BufDev acc, BufDev trunc, PktDev out);
 // First kernel of a frame: parameter block (mapped host -> device slot), counters zeroed, host ack.
+// done_ctr: a zeroed device word private to the engine (last-CTA election for the ack)
 void launch_frame_begin(cudaStream_t s, const void* src, void* dst, size_t bytes, void* counters, size_t cnt_bytes,
-                        unsigned* ack, unsigned seq, const unsigned* in_flag = nullptr, unsigned in_val = 0);
+                        unsigned* ack, unsigned seq, const unsigned* in_flag, unsigned in_val, unsigned* done_ctr);
 // copy-stream -> engine-stream handshake: *f = v (release) once the stream's prior work is done
 void launch_set_flag(cudaStream_t s, unsigned* f, unsigned v);
 
