@@ -129,3 +129,29 @@ def test_threshold_resolution(truncate, override):
     seq = netgen.pan_sequence(rng, 2, 48, 64, 4, 3, 1)
     cfg = dict(tile_size=16, default_threshold=0.02, override_net_thresholds=int(override))
     compare_engines(OracleEngine(spec, cfg), CudaEngine(spec, cfg, "exact"), spec, seq)
+
+
+@pytest.mark.timeout(300)
+def test_two_engines_share_the_gpu():
+    """Two engines (two camera streams, StreamPool) on one GPU with interleaved
+    pipelined submits: no kernel of one engine may wait on a resource the
+    other holds (regression: a flag kernel starved by polling CTAs hung
+    --streams 2), and each engine's outputs equal the engine run alone."""
+    import torch
+    rng = np.random.default_rng(37)
+    spec = _vgg_small(rng, widths=(8, 8, "P", 16, 16, "P", 32))
+    seq = netgen.pan_rotate_sequence(rng, 3, 96, 128, 6, 3, 2, 0.3, obj=True)
+    cfg = dict(tile_size=16, input_threshold=0.1, mask_dilation=4)
+    alone = CudaEngine(spec, cfg, "exact")
+    outs_ref = [alone.run_frame(f, H)[1] for f, H in seq]
+    engs = [CudaEngine(spec, cfg, "exact").e for _ in range(2)]
+    frames = [torch.from_numpy(np.ascontiguousarray(f)).pin_memory() for f, _ in seq]
+    outs = [[torch.empty(o.shape, dtype=torch.float32).pin_memory() for o in outs_ref] for _ in engs]
+    for k, (f, (_, H)) in enumerate(zip(frames, seq)):
+        for i, e in enumerate(engs):
+            e.submit_host_frame(f.data_ptr(), *f.shape, H, outs[i][k].data_ptr(), outs[i][k].numel())
+    for e in engs:
+        e.sync()
+    for i in range(len(engs)):
+        for k in range(len(seq)):
+            assert np.array_equal(outs[i][k].numpy(), outs_ref[k]), (i, k)
