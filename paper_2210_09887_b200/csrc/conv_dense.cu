@@ -844,16 +844,11 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     }
     if (p.cout_pad % p.NBD) p.NBD = 32;
     p.nNB = p.cout_pad / p.NBD;
-    // One unit per item (measured best on the C2 layers: more SMs busy, and
-    // 32-channel K-blocks amortise the per-K-block handshake); the kernel also
-    // supports two units sharing each weight stage (umax = 2).
-    // two units per weight stage (16-channel K-blocks keep accumulators + A
-    // stages within TMEM) halve the weight stream; one unit per item keeps more
-    // SMs busy and amortises the per-K-block handshake over 32 channels
-    const long long wbytes = (long long)cin * cout * k * k * 8;
-    p.umax = 1;  // measured: one unit per item wins on the C2 layers (DFX_DENSE_UMAX=2 to compare)
-    (void)wbytes;
-    if (const char* u = getenv("DFX_DENSE_UMAX")) p.umax = (atoi(u) >= 2 && p.cin_pad % 16 == 0) ? 2 : 1;
+    // One unit per item: measured best on the C2 layers (more SMs busy). Two
+    // units sharing a weight stage (umax = 2) was measured slower earlier and is
+    // not kept working with the raw patch ring / split producers, so it is not
+    // selectable.
+    p.umax = 1;
     // 16-channel K-blocks: 16 KB weight stages, a deeper ring hides the bulk-copy latency (measured +2-4%)
     p.KC = p.cin_pad % 16 == 0 ? 16 : 8;
     p.r = k / 2;
