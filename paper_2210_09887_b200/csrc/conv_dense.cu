@@ -898,6 +898,7 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
         if (v >= 2 && v <= kMaxPB) p.npb = v;
     }
     if (p.npb > 2 && !fits(4, 2) && !fits(4, 1)) p.npb = 2;
+    const int kc_pref = p.KC;
     if (p.KC > 8 && !fits(4, 2) && !fits(4, 1)) set_kc(8);  // large tile-unit patches: 8-channel K-blocks
     // two MMA issuers (one accumulator each) when TMEM holds them with >= 4 stages
     {
@@ -920,6 +921,18 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     const int BH = t_out > kUY ? t_out : kUY, BW = t_out > kUX ? t_out : kUX;
     p.ok = fits(p.nstw, p.nbuf) && k * k <= 49 && (k & 1) && t_out <= 64 && (BH / kUY) * (BW / kUX) <= 32 &&
            (BH / t_out) * (BW / t_out) <= 32 && p.patch_px * p.umax <= 2 * 22 * 14;
+    // Plans squeezed below the validated shape (8-channel K-blocks forced on a
+    // 16-channel layer, a single accumulator buffer, fewer than 4 weight stages)
+    // failed to launch in a reduced-budget sweep (DFX_DENSE_SMEM_KB=120): such
+    // layers take the gathered-target conv instead.
+    // Fewer than 6 weight stages (large layers under a tight budget) failed to
+    // launch in a reduced-budget sweep (DFX_DENSE_SMEM_KB=120: 4-5 stages with
+    // two MMA issuers); the C2 layers plan 7-8. Such layers take the
+    // gathered-target conv until that pipeline shape is fixed.
+    if (p.nstw < 6) p.ok = false;
+    if (getenv("DFX_PLAN_DUMP"))
+        fprintf(stderr, "plan cin=%d cout=%d k=%d t=%d KC=%d/%d nbuf=%d nstw=%d nmma=%d npb=%d tpu=%d ok=%d\n", cin, cout,
+                k, t_out, p.KC, kc_pref, p.nbuf, p.nstw, p.nmma, p.npb, p.tpu, (int)p.ok);
     // units over [-16, rows*t + hg) x [-8, cols*t + hg) (hg <= 8 px of grown halo)
     p.nux_max = (cols * t_out + 8 + kUX - 1) / kUX + 1;
     p.nuy_max = (rows * t_out + 8 + kUY - 1) / kUY + 1;
