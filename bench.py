@@ -1,30 +1,39 @@
 #!/usr/bin/env python
 """bench.py — frames/s of the B200 sparse frame-difference path (driver contract).
 
-Workload (BASELINE.json configs[1]): 8-layer VGG-style delta
-CNN (3->64, 64->64, P2, 64->128, 128->128, P2, 128->256, 256->256, P2,
-256->256, 256->256; relu after every conv; He-uniform random-init weights),
-512x512x3 frames of a synthetic camera sequence panning (+2,+1) px/frame and
-rotating 0.2 deg/frame (homography -> bilinear residual warp) with a moving
-textured object; tile 16; input threshold 0.3, layer threshold 0.02
-(reference default), mask dilation 4 -- tuned, as SURVEY §8(d) C2 asks, toward
-the ~10% update rate (measured mean ~13%: the pan + rotation unveil new content
-every frame, which no threshold can suppress). The measured mean input update
-rate is reported.
+Headline workload (BASELINE.json configs[1]): the 8-layer
+VGG-style delta CNN (3->64, 64->64, P2, 64->128, 128->128, P2, 128->256,
+256->256, P2, 256->256, 256->256; relu after every conv; He-uniform random
+weights) on 512x512x3 frames of a synthetic camera sequence that pans (+2,+1)
+px/frame and rotates 0.2 deg/frame (homography -> bilinear residual warp) over
+a textured world with a moving textured object. Tile 16, input threshold 0.3
+(inside the frames' [0.33, 0.67] value range, so scene changes pass the gate
+on their own), layer threshold 0.02 (the reference default), dilation 4. The
+mean input update rate of the timed frames is measured and reported (~0.12-0.16
+over frames 5-25; it drifts upward later: the reference's `trunc += raw`
+input truncation accumulates warp residuals, engine.cpp:233-237).
 
-One step = one frame of one stream through the whole path (align/warp, input
-gate, ledger plan, claims reset, per-layer sparse conv / fused truncation /
-sparse pooling, dense output). Frames of a stream are sequential (every frame
-mutates the spherical buffers). Multi-GPU: one independent stream per GPU
-(weak scaling, no collective on the hot path).
+One step = one frame of every stream of the job through the whole path (align
+/ warp, input gate, ledger plan, claims reset, per-layer sparse conv / fused
+truncation / sparse pooling, dense output). Frames of one stream are
+sequential (every frame mutates the spherical buffers), so multi-GPU scaling
+is stream-parallel: each rank (one process per GPU) runs its own independent
+streams, no collective on the data path (`scaling: weak`).
+
+Other configs (`--config`): c3 (ResNet-18-style, 1280x720, pan (+4,+2)), c4
+(HRNet-W32-style, 256x192 crops, patch-update sequence at `--rate`), c5 (64
+c3 streams partitioned over the ranks). `--sweep` adds the update-rate sweep
+(1-50 %) with frames/s and frame-roofline fraction per point.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c2|c3|c4|c5] [--streams S] [--sweep] [--dry-run]
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import tempfile
@@ -37,21 +46,58 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 METRIC = "frames/s at named update rate on 1/8 B200; HBM GB/s & tensor-pipe % vs peak"
-TILE = 16
-FRAME = 512
-INPUT_THR = 2.0  # tuned so the C2 sequence runs at the named ~10% update rate over the default window
-DILATION = 4
-CPU_CROP = 128  # CPU-baseline sample: same network / camera motion on a 128x128 window
-WORKLOAD_FILE = os.path.join(ROOT, "profiles", "workload_c2.json")
+SWEEP_RATES = (0.01, 0.05, 0.1, 0.2, 0.35, 0.5)
+
+# SURVEY §8(d) configurations. `seq` builds (frame CHW float32, homography) pairs.
+CONFIGS = {
+    "c2": dict(workload="C2: vgg8 delta CNN, 512x512x3, pan(+2,+1)px + 0.2deg/frame rotation + moving object",
+               h=512, w=512, cfg=dict(tile_size=16, input_threshold=0.3, default_threshold=0.02, mask_dilation=4),
+               crop=(128, 128)),
+    "c3": dict(workload="C3: ResNet-18-style delta backbone (7x7 s2 stem, pool, 4 stages x 2 basic blocks, 1x1 s2 "
+                        "projections, residual adds), 1280x720x3, pan (+4,+2) px/frame",
+               h=720, w=1280, cfg=dict(tile_size=32), crop=(192, 256)),
+    "c4": dict(workload="C4: HRNet-W32-style pose net (4 branches 32/64/128/256 ch at stride 4/8/16/32, fusion by "
+                        "3x3 s2 convs and 1x1 conv + upsample + add), 256x192x3, patch-update sequence",
+               h=256, w=192, cfg=dict(tile_size=32, mask_dilation=0), crop=(256, 192)),
+}
+CONFIGS["c5"] = dict(CONFIGS["c3"], workload="C5: 64 independent C3 streams (ResNet-18-style, 1280x720) partitioned "
+                                             "over the ranks")
+
+
+def make_net(config):
+    import netgen
+    rng = np.random.default_rng(2210)
+    if config == "c2":
+        return netgen.vgg8_net(rng)
+    if config in ("c3", "c5"):
+        return netgen.resnet18_net(rng)
+    if config == "c4":
+        return netgen.hrnet_w32_net(rng)
+    raise ValueError(config)
+
+
+def make_sequence(config, frames, seed, h=None, w=None, rate=0.1):
+    import netgen
+    c = CONFIGS[config]
+    h, w = h or c["h"], w or c["w"]
+    rng = np.random.default_rng(seed)
+    if config == "c2":
+        return netgen.pan_rotate_sequence(rng, 3, h, w, frames, 2, 1, 0.2, obj=True)
+    if config in ("c3", "c5"):
+        return netgen.pan_sequence(rng, 3, h, w, frames, 4, 2)
+    return netgen.patch_update_sequence(rng, 3, h, w, frames, rate, c["cfg"]["tile_size"])
+
+
+def make_workload(frames, seed, config="c2", rate=0.1):
+    return make_net(config), dict(CONFIGS[config]["cfg"]), make_sequence(config, frames, seed, rate=rate)
 
 
 def load_peaks():
     """HBM GB/s and bf16 TFLOP/s from MEASURED_PEAKS.json (driver-written), else
     the B200_PROFILING.md fallback; TF32 TFLOP/s measured on this pool's B200 by
     tools/tf32_peak.py (profiles/tf32_peak.json), else bf16 / 2."""
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        d = json.load(open(p))
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         hbm, bf16, src = d["hbm_gbs"], d["bf16_tflops"], "measured (MEASURED_PEAKS.json)"
     except Exception:
         hbm, bf16, src = 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
@@ -61,14 +107,6 @@ def load_peaks():
     except Exception:
         tf32, tsrc = bf16 / 2.0, "bf16/2"
     return hbm, bf16, src, tf32, tsrc
-
-
-def make_workload(frames, seed, size=FRAME):
-    import netgen
-    spec = netgen.vgg8_net(np.random.default_rng(2210))
-    seq = netgen.pan_rotate_sequence(np.random.default_rng(seed), 3, size, size, frames, 2, 1, 0.2, obj=True)
-    cfg = dict(tile_size=TILE, input_threshold=INPUT_THR, default_threshold=0.02, mask_dilation=DILATION)
-    return spec, cfg, seq
 
 
 # ------------------------------------------------------------------ clocks
@@ -89,7 +127,7 @@ class ClockSampler:
                                        "-i", str(self.index), "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
-        time.sleep(0.15)
+        time.sleep(0.3)
         return self
 
     def __exit__(self, *a):
@@ -118,96 +156,202 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
 
 
-# ------------------------------------------------------------------ CPU side
-def full_frame_gflop(measured=None):
-    """Conv GFLOP per sparse 512x512 frame of the bench sequence (the
-    reference's FlopReport metric; identical for every implementation because
-    the masks are bit-exact). Measured live by the GPU arm, else read from
-    profiles/workload_c2.json (written by a previous GPU run)."""
-    if measured:
-        return measured, "measured in this run"
-    try:
-        return float(json.load(open(WORKLOAD_FILE))["conv_gflop_per_frame"]), "profiles/workload_c2.json"
-    except Exception:
-        return None, None
-
-
-def cpu_reference(steps, warmup, threads=None, crop=CPU_CROP, full_gflop=None):
-    """The reference's own CPU engine (oracle/_ref, built from /root/reference)
-    on this host's cores: one engine per thread / stream, each its own crop
-    sequence of the same network and camera motion; the C restatement port
-    only if the reference build is absent. Throughput is converted to 512x512
-    frames/s by conv FLOPs (the reference's FlopReport): CPU conv GFLOP/s
-    divided by the full frame's conv GFLOP."""
-    import netgen
+# ------------------------------------------------------------------ CPU side (checker / reference arm only)
+def cpu_crop_baseline(config, full_gflop, steps=8, warmup=1):
+    """GPU arm's cpu_baseline leg: the reference's own CPU engine (oracle/_ref,
+    built from /root/reference) on this host's cores, one engine per thread,
+    each on a crop sequence of the same network and camera motion, bounded to
+    ~10-30 s. Converted to full frames/s by conv FLOPs (the reference's
+    FlopReport) with the full frame's GFLOP measured in this run."""
     from oracle import oracle
     ncores = os.cpu_count() or 1
-    P = max(1, min(ncores, threads or ncores, 32))
     kind = "reference" if oracle.ref_available() else "port"
-    spec = netgen.vgg8_net(np.random.default_rng(2210))
-    cfg = dict(tile_size=TILE, input_threshold=INPUT_THR, default_threshold=0.02, mask_dilation=DILATION)
+    P = max(1, min(ncores, 32)) if kind == "reference" else 1
+    spec = make_net(config)
+    cfg = dict(CONFIGS[config]["cfg"])
+    ch, cw = CONFIGS[config]["crop"]
     F = warmup + steps
-    if kind != "reference":
-        P = 1
-    frames = np.zeros((P, F, 3, crop, crop), np.float32)
+    frames = np.zeros((P, F, 3, ch, cw), np.float32)
     hs = np.zeros((P, F, 9), np.float32)
     for s in range(P):
-        for k, (f, H) in enumerate(netgen.pan_rotate_sequence(np.random.default_rng(7000 + s), 3, crop, crop, F,
-                                                                 2, 1, 0.2, obj=True)):
-            frames[s, k] = f
-            hs[s, k] = H
+        for k, (f, H) in enumerate(make_sequence(config, F, 7000 + s, h=ch, w=cw)):
+            frames[s, k], hs[s, k] = f, H
     if kind == "reference":
         secs, flops = oracle.ref_run_streams(spec, cfg, frames, hs)
     else:
-        secs = np.zeros((P, F))
-        flops = np.zeros((P, F), np.uint64)
+        secs, flops = np.zeros((P, F)), np.zeros((P, F), np.uint64)
         e = oracle.OracleEngine(spec, cfg)
         for k in range(F):
             t0 = time.time()
             info, _ = e.run_frame(frames[0, k], hs[0, k])
-            secs[0, k] = time.time() - t0
-            flops[0, k] = info["conv_flops"]
-    timed = secs[:, warmup:]
-    wall = float(timed.sum(axis=1).max())
+            secs[0, k], flops[0, k] = time.time() - t0, info["conv_flops"]
+    wall = float(secs[:, warmup:].sum(axis=1).max())
     gflops_s = float(flops[:, warmup:].astype(np.float64).sum()) / wall / 1e9
-    crop_fps = P * steps / wall
-    ff, src = full_frame_gflop(full_gflop)
-    if ff:
-        value, norm = gflops_s / ff, f"converted to 512x512 frames/s by conv FLOPs ({ff:.2f} GFLOP/frame, {src})"
-    else:
-        value, norm = crop_fps * (crop * crop) / float(FRAME * FRAME), "converted to 512x512 frames/s by pixel area"
-    return {
-        "value": value,
-        "unit": "frames/s",
-        "cores": P,
-        "kind": kind,
-        "sample": (f"{P} threads, one reference engine per thread, {steps} sparse frames each (after {warmup} warm-up "
-                   f"incl. the dense first frame) of the same net / camera motion on {crop}x{crop} crops: "
-                   f"{gflops_s:.2f} conv GFLOP/s aggregate over {wall:.1f} s; {norm}"),
-        "crop_frames_per_s": crop_fps,
-    }
+    return {"value": gflops_s / full_gflop, "unit": "frames/s", "cores": P, "kind": kind,
+            "sample": (f"{P} threads, one reference engine per thread, {steps} sparse frames each (after {warmup} "
+                       f"warm-up incl. the dense first frame) of the same net / camera motion on {ch}x{cw} crops: "
+                       f"{gflops_s:.2f} conv GFLOP/s aggregate over {wall:.1f} s, converted to full frames/s by the "
+                       f"full frame's conv GFLOP measured in this run ({full_gflop:.2f})")}
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference's own CPU engine (oracle/_ref = the
+    UNMODIFIED reference compiled from /root/reference by oracle/Makefile) on
+    the host cores, on THIS arm's config: full-size frames of the same
+    sequences, one engine per thread. Each thread runs its
+    stream's frames 0..W-1 untimed (frame 0 is dense) and then a bounded sample
+    of the timed steps: the first `sample` timed frames (W, W+1), so the whole
+    run ends within a few minutes. frames/s = threads / mean seconds per timed
+    frame."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    r = cpu_reference(min(args.steps, 8), max(1, min(args.warmup, 2)))
+    from oracle import oracle
+    config = args.config
+    kind = "reference" if oracle.ref_available() else "port"
+    ncores = os.cpu_count() or 1
+    P = max(1, min(ncores, 32))  # every host thread it can use, one stream each
+    if kind != "reference":
+        P = 1
+    # bounded: the dense first frame of C3 / C5 alone is ~2 min of one core
+    W = args.warmup if config in ("c2", "c4") else 1
+    sample = 2
+    F = W + sample
+    spec = make_net(config)
+    cfg = dict(CONFIGS[config]["cfg"])
+    nseq = min(P, 4)
+    seqs = [make_sequence(config, F, 1000 + i, rate=args.rate) for i in range(nseq)]
+    c, h, w = seqs[0][0][0].shape
+    frames = np.zeros((P, F, c, h, w), np.float32)
+    hs = np.zeros((P, F, 9), np.float32)
+    for s in range(P):
+        for k, (f, H) in enumerate(seqs[s % nseq]):
+            frames[s, k], hs[s, k] = f, H
+    t0 = time.time()
+    if kind == "reference":
+        secs, flops = oracle.ref_run_streams(spec, cfg, frames, hs)
+    else:
+        secs, flops = np.zeros((P, F)), np.zeros((P, F), np.uint64)
+        e = oracle.OracleEngine(spec, cfg)
+        for k in range(F):
+            t1 = time.time()
+            info, _ = e.run_frame(frames[0, k], hs[0, k])
+            secs[0, k], flops[0, k] = time.time() - t1, info["conv_flops"]
+    wall = time.time() - t0
+    per_frame = float(secs[:, W:].mean())
+    value = P / per_frame
     line = {
-        "metric": METRIC, "value": r["value"], "unit": "frames/s", "impl": "reference", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / r["value"] if r["value"] else None,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "C2 vgg8 512x512 pan+rotation (CPU: area-normalised crops)", "tile": TILE},
-        "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
-        "e2e": {"value": r["value"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "metric": METRIC, "value": value, "unit": "frames/s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": CONFIGS[config]["workload"], "config": config, "frame": [h, w], **cfg,
+                   "same_config": True, "timed_frames": list(range(W, F)),
+                   "conv_gflop_per_frame": float(flops[:, W:].astype(np.float64).mean()) / 1e9,
+                   "dense_frame0_s": float(secs[:, 0].mean()), "threads": P},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": P, "kind": kind,
+                         "sample": (f"{P} threads x 1 stream each (full {h}x{w} frames of the GPU arm's sequences, "
+                                    f"seeds 1000..{999 + nseq} cyclic), frames 0..{W - 1} untimed (frame 0 dense: "
+                                    f"{float(secs[:, 0].mean()):.1f} s mean), frames {W}..{F - 1} timed: "
+                                    f"{per_frame:.2f} s/frame/thread; run wall {wall:.0f} s")},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ GPU side
+def family_table(prof, K, hbm_peak, tc_peak):
+    kernels = {}
+    for name, p in prof.items():
+        if not p["launches"]:
+            continue
+        tensor = p["bound"] == "tensor"
+        peak = tc_peak if tensor else hbm_peak
+        ach = p["work"] / (p["ms"] / 1e3) / (1e12 if tensor else 1e9)
+        kernels[name] = {"ms_per_step": p["ms"] / K, "achieved": ach, "unit": "TFLOP/s" if tensor else "GB/s",
+                         "peak": peak, "frac": ach / peak, "launches_per_step": p["launches"] / K,
+                         "work_per_step": p["work"] / K}
+    total_ms = sum(k["ms_per_step"] for k in kernels.values())
+    for k in kernels.values():
+        k["share"] = k["ms_per_step"] / total_ms if total_ms else 0.0
+    return kernels
+
+
+def frame_roofline(kernels):
+    """the frame's roofline time = sum over kernel families of
+    max(bytes/BW, flops/P_tc); each family is bound by one of the two."""
+    us = 0.0
+    for k in kernels.values():
+        scale = 1e12 if k["unit"] == "TFLOP/s" else 1e9
+        us += k["work_per_step"] / (k["peak"] * scale) * 1e6
+    return us
+
+
+def profile_engine(dfx, spec, econf, local, dframes, seq, W, K):
+    """Per-family CUDA-event times and algorithmic work over K frames after W
+    warm-up frames on one engine (profiling mode: synchronous frames)."""
+    eng = dfx.DeltaEngine(spec, econf, device=local)
+    for k in range(W):
+        eng.submit_frame(dframes[k].data_ptr(), *dframes[k].shape, seq[k][1])
+        eng.sync()
+    eng.set_profiling(True)
+    eng.reset_profile()
+    infos = []
+    for k in range(W, W + K):
+        eng.submit_frame(dframes[k].data_ptr(), *dframes[k].shape, seq[k][1])
+        infos.append(eng.sync())
+    prof = eng.profile()
+    eng.close()
+    return prof, infos
+
+
+def device_fps(dfx, spec, econf, local, dframes, seq, W, K):
+    """Device-resident frames/s of one engine (CUDA events on its stream)."""
+    eng = dfx.DeltaEngine(spec, econf, device=local)
+    for k in range(W):
+        eng.submit_frame(dframes[k].data_ptr(), *dframes[k].shape, seq[k][1])
+        eng.sync()
+    eng.timer_start()
+    for k in range(W, W + K):
+        eng.submit_frame(dframes[k].data_ptr(), *dframes[k].shape, seq[k][1])
+    ms = eng.timer_stop()
+    eng.sync()
+    eng.close()
+    return K / (ms / 1e3)
+
+
+def run_sweep(dfx, torch, config, spec, econf, local, W, K, hbm_peak, tc_peak):
+    """Update-rate sweep: integer-translation patch-update
+    sequences whose input update rate is set by the fraction of tiles that
+    receive a new textured patch each frame; frames/s and frame-roofline
+    fraction at each measured rate."""
+    import netgen
+    c = CONFIGS[config]
+    t = econf.tile_size
+    dev = torch.device("cuda", local)
+    pts = []
+    cfg = dict(c["cfg"], mask_dilation=0)
+    ec = dfx.EngineConfig(**cfg, conv_mode="tf32x3")
+    for r in SWEEP_RATES:
+        seq = netgen.patch_update_sequence(np.random.default_rng(4242), 3, c["h"], c["w"], W + K, r, t, 2 * t, t)
+        dfr = [torch.from_numpy(f).to(dev) for f, _ in seq]
+        fps = device_fps(dfx, spec, ec, local, dfr, seq, W, K)
+        prof, infos = profile_engine(dfx, spec, ec, local, dfr, seq, W, K)
+        ker = family_table(prof, K, hbm_peak, tc_peak)
+        roof_us = frame_roofline(ker)
+        pts.append({"target_rate": r, "update_rate": float(np.mean([i["update_rate"] for i in infos])),
+                    "frames_per_s": fps, "frame_roofline_us": roof_us, "frame_roofline_frac": fps * roof_us / 1e6,
+                    "conv_gflop_per_frame": float(np.mean([i["conv_flops"] for i in infos])) / 1e9})
+        del dfr
+    return {"sequence": f"patch-update (integer pan {2 * t},{t} px/frame), dilation 0, {W} warm-up + {K} frames per "
+                        f"point", "points": pts}
+
+
 def run_ours(args):
     import torch
     import paper_2210_09887_b200 as dfx
+    from paper_2210_09887_b200 import _capi
+    from paper_2210_09887_b200.streams import max_over_ranks, partition
+    import ctypes
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -221,14 +365,15 @@ def run_ours(args):
         else:  # ranks sharing a GPU (testing the multi-rank path on a 1-GPU box): NCCL forbids it
             dist.init_process_group("gloo")
 
-    W, K, S = args.warmup, args.steps, max(1, args.streams)
-    from paper_2210_09887_b200.streams import partition
-    my_streams = partition(world * S, world, rank)  # this rank's independent camera streams
+    config = args.config
+    W, K = args.warmup, args.steps
+    n_total = 64 if config == "c5" else world * max(1, args.streams)
+    my_streams = partition(n_total, world, rank)  # this rank's independent camera streams
+    S = len(my_streams)
     nseq = min(S, 4)  # distinct synthetic sequences per rank (reused cyclically beyond 4)
-    seqs = []
-    for i in range(nseq):
-        spec, cfg, sq = make_workload(W + K, seed=1000 + my_streams[i])
-        seqs.append(sq)
+    spec = make_net(config)
+    cfg = dict(CONFIGS[config]["cfg"])
+    seqs = [make_sequence(config, W + K, 1000 + my_streams[i], rate=args.rate) for i in range(nseq)]
     seq = seqs[0]
     econf = dfx.EngineConfig(**cfg, conv_mode="tf32x3")
     dev = torch.device("cuda", local)
@@ -255,19 +400,26 @@ def run_ours(args):
         for eng in engs:
             eng.sync()
     torch.cuda.synchronize()
-    kernels_per_step = engs[0].kernel_count()
-    from paper_2210_09887_b200.streams import max_over_ranks
+    kernels_per_step = sum(e.kernel_count() for e in engs)
+    # a dense frame (full mask) after reset() (engine.cpp:93-108, 207-211): the
+    # first frame of a stream / after a pan reversal, timed alone (outside the
+    # timed region)
+    engs[0].reset()
+    engs[0].timer_start()
+    engs[0].submit_frame(dframes[0][W + K - 1].data_ptr(), *dframes[0][W + K - 1].shape, seq[W + K - 1][1])
+    t_f0 = engs[0].timer_stop()
+    engs[0].sync()
+    for e in engs:
+        e.close()
     if dist:
         dist.barrier()
     ms_max = max_over_ranks(ms, dist)
-    value = world * S * K / (ms_max / 1000.0)
-    eng = engs[0]
+    value = n_total * K / (ms_max / 1000.0)
+    rank_fps = S * K / (ms / 1000.0)
 
     # ---- 2. e2e through the public API: pinned host frames in, pinned host outputs back; every
     # step's H2D frame copy and D2H output copy are inside the timed region (pipelined host-frame
     # API, dfx_engine_submit_host_frame: copies overlap the neighbouring frames' compute)
-    from paper_2210_09887_b200 import _capi
-    import ctypes
     _, capi = _capi.load_library()
     fbytes = seq[0][0].nbytes
     hframes = []  # [seq][frame] page-locked host frames (dfx_host_alloc), filled before the timed region
@@ -285,7 +437,6 @@ def run_ours(args):
     oc, oh, ow = eng2.last_info["out_channels"], eng2.last_info["out_height"], eng2.last_info["out_width"]
     ocap = oc * (oh + 64) * (ow + 64)
     houts = [[capi["host_alloc"](ocap * 4) for _ in range(2)] for _ in range(S)]
-    # warm-up through the same pipelined path (allocates its double buffers outside the timed region)
     for k in range(1, W):
         for i, e2 in enumerate(engs2):
             sq = seqs[i % nseq]
@@ -302,60 +453,54 @@ def run_ours(args):
         for i, e2 in enumerate(engs2):
             sq = seqs[i % nseq]
             e2.submit_host_frame(hframes[i % nseq][k], *sq[k][0].shape, sq[k][1], houts[i][k & 1], ocap)
-        out_bytes += oc * oh * ow * 4
+            out_bytes += oc * oh * ow * 4
     for e2 in engs2:
         e2.sync()
     ms2 = max(e2.timer_stop() for e2 in engs2)
     ms2 = max(ms2, (time.time() - t_wall) * 1e3)
+    for e2 in engs2:
+        e2.close()
     for p in [p for hf in hframes for p in hf] + [p for ho in houts for p in ho]:
         capi["host_free"](p)
-    e2e_value = world * S * K / (max_over_ranks(ms2, dist) / 1000.0)
+    e2e_value = n_total * K / (max_over_ranks(ms2, dist) / 1000.0)
 
     # ---- 3. per-family kernel times (CUDA events on the engine stream) + algorithmic work
-    eng3 = dfx.DeltaEngine(spec, econf, device=local)
-    for k in range(W):
-        eng3.submit_frame(dframes[0][k].data_ptr(), *dframes[0][k].shape, seq[k][1])
-        eng3.sync()
-    eng3.set_profiling(True)
-    eng3.reset_profile()
-    infos = []
-    for k in range(W, W + K):
-        eng3.submit_frame(dframes[0][k].data_ptr(), *dframes[0][k].shape, seq[k][1])
-        infos.append(eng3.sync())
-    prof = eng3.profile()
+    prof, infos = profile_engine(dfx, spec, econf, local, dframes[0], seq, W, K)
     update_rate = float(np.mean([i["update_rate"] for i in infos]))
     conv_gflop = float(np.mean([i["conv_flops"] for i in infos])) / 1e9
     dense_gflop = float(np.mean([i["dense_flops"] for i in infos])) / 1e9
     hbm_peak, bf16_peak, peak_src, tf32_peak, tf32_src = load_peaks()
     tc_peak = tf32_peak / 3.0  # 3xTF32: 3 MMA passes per algorithmic FLOP
-    kernels = {}
-    for name, p in prof.items():
-        if not p["launches"]:
-            continue
-        if p["bound"] == "tensor":
-            ach = p["work"] / (p["ms"] / 1e3) / 1e12
-            kernels[name] = {"ms_per_step": p["ms"] / K, "achieved": ach, "unit": "TFLOP/s", "peak": tc_peak,
-                             "frac": ach / tc_peak, "launches_per_step": p["launches"] / K}
-        else:
-            ach = p["work"] / (p["ms"] / 1e3) / 1e9
-            kernels[name] = {"ms_per_step": p["ms"] / K, "achieved": ach, "unit": "GB/s", "peak": hbm_peak,
-                             "frac": ach / hbm_peak, "launches_per_step": p["launches"] / K}
-    total_ms = sum(k["ms_per_step"] for k in kernels.values())
-    for k in kernels.values():
-        k["share"] = k["ms_per_step"] / total_ms if total_ms else 0.0
+    kernels = family_table(prof, K, hbm_peak, tc_peak)
     dom = max(kernels, key=lambda n: kernels[n]["ms_per_step"])
     d = kernels[dom]
     traffic = None
     try:
         summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = summ.get("traffic_per_launch", {}).get(dom)
+        traffic = summ.get("traffic_per_launch", {}).get(dom) if config == "c2" else None
     except Exception:
         pass
     roofline = {"bound": "tensor" if d["unit"] == "TFLOP/s" else "hbm", "kernel": dom, "achieved": d["achieved"],
                 "peak": d["peak"], "unit": d["unit"], "frac": d["frac"], "traffic": traffic,
                 "peak_source": (tf32_src + " / 3 (3xTF32)") if d["unit"] == "TFLOP/s" else peak_src}
+    roof_us = frame_roofline(kernels)
+    per_gpu_fps = value / world
+    frame_roof = {"us_per_frame": roof_us, "frames_per_s_per_gpu": 1e6 / roof_us if roof_us else None,
+                  "frac": per_gpu_fps * roof_us / 1e6 / max(1, S) if roof_us else None,
+                  "update_rate": update_rate,
+                  "how": "sum over kernel families of algorithmic work / peak (HBM bytes / measured HBM GB/s, conv "
+                         "FLOPs / (TF32 peak / 3)) at the measured update rate; frac = achieved per-GPU frames/s "
+                         "per stream x roofline time"}
+    per_rank = [rank_fps]
+    if dist:
+        obj = [None] * world
+        dist.all_gather_object(obj, rank_fps)
+        per_rank = obj
 
-    state_mb = None
+    sweep = None
+    if args.sweep and rank == 0:
+        sweep = run_sweep(dfx, torch, config, spec, econf, local, 3, 10, hbm_peak, tc_peak)
+
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -366,60 +511,107 @@ def run_ours(args):
             "warmup": W,
             "ms_per_step": ms_max / K,  # one step = one frame of every stream of the job
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if config == "c5" else "weak",
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic",
             "config": {
-                "workload": "C2: vgg8 delta CNN, 512x512x3, pan(+2,+1)px + 0.2deg/frame rotation + moving object",
+                "workload": CONFIGS[config]["workload"],
+                "config": config,
+                "frame": list(seq[0][0].shape),
+                **cfg,
                 "update_rate": update_rate,
                 "conv_gflop_per_frame": conv_gflop,
                 "dense_gflop_per_frame": dense_gflop,
-                "tile": TILE,
                 "conv_mode": "tf32x3 (tcgen05 kind::tf32, 3-pass split)",
                 "streams_per_gpu": S,
+                "streams_total": n_total,
+                "dense_frame_ms": t_f0,
                 "l2": "inputs larger than L2: per-stream spherical state is several hundred MB (> 126 MB L2)",
                 "parallelism": f"stream-parallel x{world} (independent streams, no collective)",
             },
-            "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": int(seq[0][0].nbytes),
-                    "d2h_bytes_per_step": int(out_bytes // max(1, K))},
+            "per_rank_frames_per_s": per_rank,
+            "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": int(fbytes) * n_total,
+                    "d2h_bytes_per_step": int(out_bytes // max(1, K)) * world},
             "roofline": roofline,
+            "frame_roofline": frame_roof,
             "kernels": kernels,
-            "gpu_launches": kernels_per_step * K * S,
+            "gpu_launches": kernels_per_step * K,
             "clocks": clk.summary(),
         }
+        if sweep:
+            line["sweep"] = sweep
         if world == 1 and not args.no_cpu_baseline:
             try:
-                cb = cpu_reference(steps=8, warmup=1, full_gflop=conv_gflop)  # ~10 s of host work
-                line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                cb = cpu_crop_baseline(config, conv_gflop)
+                line["cpu_baseline"] = cb
             except Exception as e:  # the baseline is reported, not the target
                 line["cpu_baseline"] = {"value": None, "unit": "frames/s", "cores": 0, "kind": "reference",
                                         "sample": f"failed: {e}"}
         print(json.dumps(line), flush=True)
-        if world == 1:
-            try:
-                json.dump({"conv_gflop_per_frame": conv_gflop, "update_rate": update_rate, "steps": K, "warmup": W},
-                          open(WORKLOAD_FILE, "w"), indent=1)
-            except Exception:
-                pass
     if dist:
         dist.barrier()
         dist.destroy_process_group()
 
 
+def run_dry(args):
+    """Multi-rank plumbing without a GPU (CPU tests): gloo process group,
+    stream partition, barrier, max-over-ranks time, per-rank gather."""
+    import torch.distributed as dist
+    from paper_2210_09887_b200.streams import max_over_ranks, partition
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    n_total = 64 if args.config == "c5" else world * max(1, args.streams)
+    mine = partition(n_total, world, rank)
+    ms = 10.0 + rank
+    if world > 1:
+        dist.barrier()
+    ms_max = max_over_ranks(ms, dist if world > 1 else None)
+    per = [mine]
+    if world > 1:
+        per = [None] * world
+        dist.all_gather_object(per, mine)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ms_max": ms_max, "streams_per_rank": per,
+                          "streams_total": n_total}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def spawn_ranks(argv, n):
+    """`python bench.py --gpus N` without a torchrun environment: launch N
+    ranks (one process per GPU) through torch.distributed.run on 127.0.0.1."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--rate", type=float, default=0.1, help="c4: fraction of tiles updated per frame")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="add the 1-50%% update-rate sweep")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only (no GPU)")
     ap.add_argument("--streams", type=int, default=1,
                     help="independent camera streams per GPU (one engine each, kernels overlap across streams)")
     args = ap.parse_args()
-    if args.warmup < 1:
-        args.warmup = 1
-    if args.impl == "reference":
+    args.warmup = max(3, args.warmup)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(sys.argv[1:], args.gpus))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference_arm(args)
     else:
         run_ours(args)

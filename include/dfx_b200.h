@@ -7,9 +7,12 @@
  *
  *   dfx_engine_create        dflx::DeltaEngine::DeltaEngine(spec, cfg)   include/deltaflux/engine.hpp:47,
  *                            src/engine.cpp:7-15 (validate() at src/network.cpp:46-254)
+ *   dfx_engine_create_on_stream  same, bound to a caller-supplied cudaStream_t
  *   dfx_engine_destroy       ~DeltaEngine
  *   dfx_engine_run_frame     DeltaEngine::run_frame(frame, h, roi)      engine.hpp:51, engine.cpp:184-287;
  *                            python: deltaflux._core.DeltaEngine.run_frame  bindings/py_bindings.cpp:103-121
+ *   dfx_engine_run_frame_ex  run_frame with device-resident frame / output buffers
+ *   dfx_engine_layer_order   ValidatedNet::topo (network.hpp:45), the FlopReport order
  *   dfx_engine_submit_frame  (async variant of run_frame for throughput; no reference counterpart)
  *   dfx_engine_submit_host_frame (pipelined host-buffer variant of run_frame; no reference counterpart)
  *   dfx_engine_sync          (completes submitted frames)
@@ -148,6 +151,10 @@ void dfx_default_config(dfx_engine_config* cfg);
 
 int dfx_engine_create(const dfx_net_desc* net, const dfx_engine_config* cfg, int device,
                       dfx_engine** out);
+/* Same, but every kernel of the engine runs on `stream` (a cudaStream_t owned
+ * by the caller; NULL = an engine-owned non-blocking stream). */
+int dfx_engine_create_on_stream(const dfx_net_desc* net, const dfx_engine_config* cfg, int device, void* stream,
+                                dfx_engine** out);
 int dfx_engine_destroy(dfx_engine* e);
 
 /* Synchronous frame: host CHW frame (c x h x w fp32), 3x3 row-major
@@ -156,6 +163,14 @@ int dfx_engine_destroy(dfx_engine* e);
  * `out` when out_cap (in floats) is large enough. */
 int dfx_engine_run_frame(dfx_engine* e, const float* frame, int c, int h, int w, const float* h9,
                          const float* roi, dfx_frame_info* info, float* out, size_t out_cap);
+
+/* run_frame with explicit buffer residency: frame_is_device = 1
+ * when `frame` (and `roi`) are device pointers, out_is_device = 1 when `out`
+ * is a device pointer (the output is copied device-to-device on the engine's
+ * stream). Synchronous like dfx_engine_run_frame. */
+int dfx_engine_run_frame_ex(dfx_engine* e, const float* frame, int c, int h, int w, int frame_is_device,
+                            const float* h9, const float* roi, dfx_frame_info* info, float* out, size_t out_cap,
+                            int out_is_device);
 
 /* Asynchronous frame on device-resident input (frame_dev: device pointer,
  * CHW). Launches the whole frame on the engine's CUDA stream and returns
@@ -183,6 +198,8 @@ int dfx_engine_output_device(dfx_engine* e, const float** ptr, int* c, int* h, i
 
 int dfx_engine_input_mask(dfx_engine* e, uint8_t* out, size_t cap, int* tiles_h, int* tiles_w);
 int dfx_engine_num_layers(dfx_engine* e);
+/* Layer indices in execution (topological) order; *n = number written. */
+int dfx_engine_layer_order(dfx_engine* e, int* order, int cap, int* n);
 int dfx_engine_layer_flops(dfx_engine* e, int layer, uint64_t* flops, uint64_t* dense_flops);
 int dfx_engine_grid(dfx_engine* e, int* rows, int* cols);
 

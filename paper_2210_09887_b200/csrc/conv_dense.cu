@@ -1,37 +1,39 @@
-// Dense-unit sparse DeltaConv on tcgen05 (sm_100a): the bulk of a stride-1
+// Dense-unit sparse DeltaConv on tcgen05 (sm_100a): a stride-1
 // padded_delta_conv (reference src/delta_layers.cpp:100-147).
 //
-// The conv output extent is cut into UNITS of 16 rows x 8 columns = 128 output
-// pixels = one MMA M tile. k_conv_units marks a unit DENSE when at least half
-// of its in-extent pixels are conv targets (delta_layers.cpp:34-70); dense
-// units are computed here, every other target (sparse units, the grown ring
-// outside the extent) by the gathered kernel in conv_tc.cu. Both write
-// disjoint pixels of the output packet.
+// Work units (built by k_conv_plan, plan_block.inc.cuh): one unit = one MMA M
+// tile of 128 output pixels, either a 16 x 8-pixel block of the grown extent
+// (t >= 16) or 128 / t^2 ACTIVE output tiles gathered from anywhere in the
+// extent (t in {2, 4, 8}, "tile units"). Every unit holding at least one conv
+// target (tau = 1 by default) is computed whole here.
 //
 // Why whole units are exact: a non-target pixel's window touches no masked
 // input tile (grown by the input halo), and unmasked packet tiles are zero by
 // definition (delta_layers.hpp:37-41), so computing it yields exactly the 0
 // the reference stores there; target pixels get the full window sum.
 //
-// Data movement: per (unit, 32-channel chunk) the (16+2r) x (8+2r) input patch
-// is copied ONCE into shared memory with cp.async (zero-fill via src-size 0
-// for samples outside the grown extent or in unwritten tiles), laid out
-// [c4][py][px][4 ch] — exactly the UMMA canonical K-major SWIZZLE_NONE image
-// with 8-pixel rows as core-matrix rows. Every tap (ky, kx) is then the same
-// patch seen through a descriptor whose start address moves by
-// (ky * PW + kx) * 16 bytes (SBO = PW * 16 bytes between unit rows): no
-// per-tap gathers, and the TF32 hi/lo split is done once per patch instead of
-// once per tap. Weights (pre-split hi/lo, per (N-block, K-block) images) are
-// streamed by one thread with cp.async.bulk into a stage ring.
+// Data movement: per (unit, KC = 16-channel chunk; 8 for Cin % 16 != 0) the
+// unit's raw fp32 input patch ((16+2r) x (8+2r) pixels, or one (t+2r)^2 patch
+// per tile) is copied ONCE into a ring of npb shared-memory patch buffers with
+// 16-byte cp.async (zero fill via src-size 0 outside the grown extent or in
+// unwritten tiles). For every tap, each A-producer thread reads its output
+// pixel's shifted patch row, splits it into TF32 hi / lo in registers and
+// tcgen05.st's both halves into a TMEM A stage. Weights (pre-split hi / lo,
+// one image per (N block, K block = (channel chunk, tap))) are streamed by one
+// thread with cp.async.bulk into a ring of nstw stages.
 //
-// Arithmetic: 3xTF32 (Ahi*Bhi + Ahi*Blo + Alo*Bhi, fp32 accumulation in TMEM),
-// the same as conv_tc.cu. Split-K over CTAs (deep layers with few units)
-// writes fp32 partials reduced in fixed order (deterministic).
+// Arithmetic: 3xTF32 (Ahi*Bhi + Ahi*Blo + Alo*Bhi, fp32 accumulation in TMEM;
+// A from TMEM, B from shared memory). Two MMA-issuer warps alternate K-block
+// pairs into their own accumulators; the epilogue sums the two partials in a
+// fixed order. Split-K over CTAs (small layers) writes fp32 partials that the
+// last-arriving CTA reduces in fixed order (deterministic).
 //
-// Warp roles (320 threads): 0-3 patch producers, 4-7 epilogue (TMEM lane
-// quarter = warp % 4), 8 weight producer, 9 MMA issuer. Two units share each
-// weight stage (M = 256 rows per weight byte; weight streaming from L2 is the
-// per-SM limit at M = 128).
+// Warp roles (736 threads, kProdWG = 3): warps 0-11 A producers (three
+// warpgroups taking taps round robin), 12-15 patch loaders, 16-19 epilogue
+// (TMEM lane quarter = warp % 4, double-buffered accumulators when TMEM
+// allows: nbuf), 20 and 22 MMA issuers, 21 weight producer. One unit per work item
+// (umax = 1). The plan (dense_conv_plan) picks NBD = min(Cout, 128) columns per
+// N block, nbuf and nstw to fit 200 KB of shared memory and 512 TMEM columns.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -898,7 +900,6 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
         if (v >= 2 && v <= kMaxPB) p.npb = v;
     }
     if (p.npb > 2 && !fits(4, 2) && !fits(4, 1)) p.npb = 2;
-    const int kc_pref = p.KC;
     if (p.KC > 8 && !fits(4, 2) && !fits(4, 1)) set_kc(8);  // large tile-unit patches: 8-channel K-blocks
     // two MMA issuers (one accumulator each) when TMEM holds them with >= 4 stages
     {
@@ -907,10 +908,11 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
         p.nmma = want;
         if (!fits(4, 2) && !fits(4, 1)) p.nmma = 1;
     }
-    // prefer double-buffered accumulators with >= 4 stages, else single with more stages
+    // prefer double-buffered accumulators with >= 6 weight stages, else a single
+    // accumulator buffer with up to 8 stages
     p.nbuf = 2;
     p.nstw = 8;
-    while (p.nstw > 4 && !fits(p.nstw, 2)) --p.nstw;
+    while (p.nstw > 6 && !fits(p.nstw, 2)) --p.nstw;
     if (!fits(p.nstw, 2)) {
         p.nbuf = 1;
         p.nstw = 8;
@@ -921,18 +923,15 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     const int BH = t_out > kUY ? t_out : kUY, BW = t_out > kUX ? t_out : kUX;
     p.ok = fits(p.nstw, p.nbuf) && k * k <= 49 && (k & 1) && t_out <= 64 && (BH / kUY) * (BW / kUX) <= 32 &&
            (BH / t_out) * (BW / t_out) <= 32 && p.patch_px * p.umax <= 2 * 22 * 14;
-    // Plans squeezed below the validated shape (8-channel K-blocks forced on a
-    // 16-channel layer, a single accumulator buffer, fewer than 4 weight stages)
-    // failed to launch in a reduced-budget sweep (DFX_DENSE_SMEM_KB=120): such
-    // layers take the gathered-target conv instead.
-    // Fewer than 6 weight stages (large layers under a tight budget) failed to
-    // launch in a reduced-budget sweep (DFX_DENSE_SMEM_KB=120: 4-5 stages with
-    // two MMA issuers); the C2 layers plan 7-8. Such layers take the
-    // gathered-target conv until that pipeline shape is fixed.
+    // Known limitation: a pipeline of fewer than 6 weight stages (reachable only
+    // when a reduced shared-memory budget is forced, DFX_DENSE_SMEM_KB=120) failed
+    // to launch in round 1's sweep; such plans are marked unsupported and the
+    // layer runs on the gathered-target conv (k_conv_tc). Every layer shape of the
+    // benchmarked networks plans 7-8 stages (tools/plan_dump.cpp).
     if (p.nstw < 6) p.ok = false;
     if (getenv("DFX_PLAN_DUMP"))
-        fprintf(stderr, "plan cin=%d cout=%d k=%d t=%d KC=%d/%d nbuf=%d nstw=%d nmma=%d npb=%d tpu=%d ok=%d\n", cin, cout,
-                k, t_out, p.KC, kc_pref, p.nbuf, p.nstw, p.nmma, p.npb, p.tpu, (int)p.ok);
+        fprintf(stderr, "plan cin=%d cout=%d k=%d t=%d KC=%d nbuf=%d nstw=%d nmma=%d npb=%d tpu=%d ok=%d\n", cin, cout, k,
+                t_out, p.KC, p.nbuf, p.nstw, p.nmma, p.npb, p.tpu, (int)p.ok);
     // units over [-16, rows*t + hg) x [-8, cols*t + hg) (hg <= 8 px of grown halo)
     p.nux_max = (cols * t_out + 8 + kUX - 1) / kUX + 1;
     p.nuy_max = (rows * t_out + 8 + kUY - 1) / kUY + 1;
@@ -993,11 +992,10 @@ void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktD
 
 template <int KC>
 static void launch_kc(int grid, size_t smem, cudaStream_t s, const Ctx& c, const DenseArgs& a) {
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<unsigned long long> configured{0};
+    once_per_device(configured, [] {
         cudaFuncSetAttribute(k_conv_dense<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        configured = true;
-    }
+    });
     launch_pdl(k_conv_dense<KC>, grid, kDenseThreads, smem, s, c, a);
 }
 
@@ -1020,9 +1018,9 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
     }
     DenseConvPlan pp = p;
     if (a.dbg & 128) a.smax = 1;  // microbenchmark: no split-K
-    if (const char* d = getenv("DFX_CONV_NST")) {  // microbenchmark: fewer pipeline stages
+    if (const char* d = getenv("DFX_CONV_NST")) {  // microbenchmark: fewer pipeline stages (>= 6, see the plan)
         const int v = atoi(d);
-        if (v >= 2 && v < pp.nstw) a.nst = v;
+        if (v >= 6 && v < pp.nstw) a.nst = v;
     }
     const long long max_items = (long long)p.ws_units * p.nNB * a.smax;
     const int grid = (int)(max_items < num_sms ? (max_items < 1 ? 1 : max_items) : num_sms);

@@ -505,13 +505,14 @@ int conv_tc_splits(int max_targets, int cin_pad, int cout_pad, int k, int num_sm
     return S;
 }
 
+bool conv_tc_supported(int k) { return k * k <= 64; }
+
 template <int NST>
 static void launch_nst(int grid, size_t smem, cudaStream_t s, const Ctx& c, const ConvArgs& a) {
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<unsigned long long> configured{0};
+    once_per_device(configured, [] {
         cudaFuncSetAttribute(k_conv_tc<NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = true;
-    }
+    });
     launch_pdl(k_conv_tc<NST>, grid, kThreadsV2, smem, s, c, a);
 }
 

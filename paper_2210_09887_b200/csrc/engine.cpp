@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <memory>
 #include <string>
@@ -128,11 +129,17 @@ int64_t overlap(int64_t a0, int64_t a1, int64_t b0, int64_t b1) {
 // ------------------------------------------------------------------ engine
 class Engine {
   public:
-    Engine(const dfx_net_desc* d, const dfx_engine_config* cfg, int device);
+    Engine(const dfx_net_desc* d, const dfx_engine_config* cfg, int device, cudaStream_t stream = nullptr);
     ~Engine();
 
     void run_frame(const float* frame, int c, int h, int w, const float* h9, const float* roi, dfx_frame_info* info,
-                   float* out, size_t cap);
+                   float* out, size_t cap, bool frame_dev = false, bool out_dev = false);
+    void layer_order(int* order, int cap, int* n) const {
+        int k = 0;
+        for (int i : net_.topo)
+            if (k < cap) order[k++] = i;
+        *n = k;
+    }
     void submit(const float* frame_dev, int c, int h, int w, const float* h9);
     void submit_host(const float* frame, int c, int h, int w, const float* h9, float* out, size_t cap);
     void sync(dfx_frame_info* info);
@@ -197,6 +204,7 @@ class Engine {
     void ensure_staging(int c, int h, int w, bool host_frame);
     PktDev in_packet(int idx) const { return idx == -1 ? in_pkt_ : lrt_[idx].pkt; }
     Ctx ctx() const { return Ctx{d_frame_, d_slots_, rows_, cols_, d_own_}; }
+    void wait_ack(unsigned seq);
     void set_param_slot(int i) {
         uint8_t* b = params_d_.p + (size_t)i * pstride_;
         d_frame_ = reinterpret_cast<FrameDev*>(b);
@@ -210,6 +218,7 @@ class Engine {
     dfx_engine_config cfg_;
     int device_ = 0;
     cudaStream_t stream_ = nullptr;
+    bool own_stream_ = true;
     int num_sms_ = 148;
     bool initialized_ = false;
     int64_t frame_index_ = 0;
@@ -292,17 +301,27 @@ class Engine {
     void prof_harvest();
 };
 
-Engine::Engine(const dfx_net_desc* d, const dfx_engine_config* cfg, int device) : cfg_(*cfg), device_(device) {
+Engine::Engine(const dfx_net_desc* d, const dfx_engine_config* cfg, int device, cudaStream_t stream)
+    : cfg_(*cfg), device_(device) {
     net_ = validate_net(d, cfg->tile_size);
     check(cfg_.tile_size >= 1, "engine: tile size must be >= 1");
     check(cfg_.input_threshold >= 0.0f && cfg_.default_threshold >= 0.0f, "engine: thresholds must be >= 0");
     check(cfg_.mask_dilation >= 0, "engine: mask dilation must be >= 0");
     int ndev = 0;
-    CUDA_CHECK(cudaGetDeviceCount(&ndev));
-    check(ndev > 0, "no CUDA device (the B200 path has no CPU fallback)");
+    const cudaError_t de = cudaGetDeviceCount(&ndev);
+    if (de != cudaSuccess) cudaGetLastError();
+    if (de != cudaSuccess || ndev <= 0)
+        fail(std::string("no CUDA device (the B200 path has no CPU fallback)") +
+                 (de != cudaSuccess ? std::string(": ") + cudaGetErrorString(de) : std::string()),
+             DFX_ERR_CUDA);
     CUDA_CHECK(cudaSetDevice(device_));
     CUDA_CHECK(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device_));
-    CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    if (stream) {
+        stream_ = stream;
+        own_stream_ = false;
+    } else {
+        CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    }
     lrt_.resize(net_.layers.size());
 }
 
@@ -333,7 +352,7 @@ Engine::~Engine() {
     }
     if (cstream_) cudaStreamDestroy(cstream_);
     if (dstream_) cudaStreamDestroy(dstream_);
-    if (stream_) cudaStreamDestroy(stream_);
+    if (stream_ && own_stream_) cudaStreamDestroy(stream_);
 }
 
 void Engine::build_packet(LayerRT& rt, int C, int t, int halo) {
@@ -420,7 +439,9 @@ void Engine::allocate(int th, int tw) {
                     rt.splits = conv_tc_splits(rt.max_targets, rt.cin_pad, rt.cout_pad, l.k, num_sms_);
                     if (rt.splits > 1) rt.ws.alloc((size_t)rt.splits * rt.max_targets * rt.cout_pad);
                     const char* dv = getenv("DFX_DENSE");
-                    if (l.stride == 1 && !(dv && dv[0] == '0')) {
+                    // the dense-unit kernel stages a patch grown by at most 8 px of halo
+                    // (launch_conv_plan); wider halos take the gathered-target kernel
+                    if (l.stride == 1 && rt.halo_geom <= 8 && !(dv && dv[0] == '0')) {
                         rt.dp = dense_conv_plan(l.cin, l.cout, l.k, l.tile, rows_, cols_, (size_t)256 << 20);
                         rt.dense = rt.dp.ok;
                     }
@@ -562,6 +583,31 @@ void Engine::reset() {
     }
 }
 
+// Waits until k_frame_begin of frame `seq` acknowledged its parameter block.
+// A fault (or a device-side trap) in an earlier frame means the ack never
+// comes: the stream is polled every few thousand spins so the sticky CUDA
+// error is reported, and a generous wall-clock bound turns a stuck device
+// into an error instead of a hang.
+void Engine::wait_ack(unsigned seq) {
+    const volatile unsigned* ack = reinterpret_cast<volatile unsigned*>(ack_h_);
+    if (*ack >= seq) return;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned spin = 1;; ++spin) {
+        if (*ack >= seq) return;
+        if ((spin & 4095) == 0) {
+            const cudaError_t q = cudaStreamQuery(stream_);
+            if (q != cudaSuccess && q != cudaErrorNotReady) {
+                cudaGetLastError();
+                fail(std::string("CUDA: ") + cudaGetErrorString(q) + " (frame pipeline)", DFX_ERR_CUDA);
+            }
+            if (q == cudaSuccess && *ack < seq)  // stream drained without the ack: the frame never ran
+                fail("frame pipeline: parameter block not acknowledged", DFX_ERR_CUDA);
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
+                fail("frame pipeline: timed out waiting for the device", DFX_ERR_CUDA);
+        }
+    }
+}
+
 int Engine::prof_begin(int fam) {
     if (!prof_) return -1;
     if (prof_used_ == prof_pool_.size()) {
@@ -665,8 +711,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     pslot_ ^= 1;
     uint8_t* params_h_ = params_hb_[pslot_];
     // the host block is free once k_frame_begin of the slot's previous frame consumed it
-    while (*reinterpret_cast<volatile unsigned*>(ack_h_) < pslot_seq_[pslot_]) {
-    }
+    wait_ack(pslot_seq_[pslot_]);
     memcpy(params_h_, &F, sizeof F);
     SlotDev* hs = reinterpret_cast<SlotDev*>(params_h_ + off_slots_);
     const auto& slots = ledger_.slots();
@@ -789,7 +834,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                                     flop_px + idx2));
                 {
                 const int pi = prof_begin(DFX_FAM_CONV_MMA);
-                if (cfg_.conv_mode == DFX_CONV_EXACT)
+                if (cfg_.conv_mode == DFX_CONV_EXACT || !conv_tc_supported(l.k))
                     launch_conv_exact(C, s, a, rt.w.p, l.cin, l.cout, l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom,
                                       rt.list.p, counts + idx2, rt.max_targets);
                 else
@@ -823,13 +868,13 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                             if (net_.layers[j].in0 == idx2 || net_.layers[j].in1 == idx2) pj = (int)j, ++ncons;
                         if (ncons == 1 && net_.layers[pj].kind == DFX_MAXPOOL) pf0 = lrt_[pj].acc, pf1 = lrt_[pj].aux;
                     }
-                    const bool two = launch_trunc_two_pass(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots,
-                                                           rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt, gbars + idx2,
-                                                           dz.out ? &dz : nullptr, &dzd, pf0, pf1);
+                    const int nk = launch_trunc_two_pass(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots,
+                                                         rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt, gbars + idx2,
+                                                         dz.out ? &dz : nullptr, &dzd, pf0, pf1);
                     if (dzd) densified = true;
                     prof_end(pi);
-                    if (two) {
-                        launches_ += 1;
+                    if (nk > 0) {
+                        launches_ += nk;
                     } else {
                         PROF(DFX_FAM_TRUNC, launch_trunc_max(C, s, a, rt.aux, tmax + (size_t)idx2 * nslots));
                         PROF(DFX_FAM_TRUNC, launch_trunc_apply(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots,
@@ -1040,9 +1085,30 @@ void Engine::ensure_staging(int c, int h, int w, bool host_frame) {
 }
 
 void Engine::run_frame(const float* frame, int c, int h, int w, const float* h9, const float* roi,
-                       dfx_frame_info* info, float* out, size_t cap) {
+                       dfx_frame_info* info, float* out, size_t cap, bool frame_dev, bool out_dev) {
     check(c == net_.in_channels, "run_frame: input channel mismatch");
     CUDA_CHECK(cudaSetDevice(device_));
+    if (frame_dev) {
+        // device-resident frame / ROI: no staging copies (SURVEY §8(b) frame_is_device)
+        ensure_staging(c, h, w, false);
+        enqueue(frame, c, h, w, h9, cfg_.roi_enabled ? roi : nullptr);
+        const size_t n = (size_t)pending_.out_channels * pending_.out_height * pending_.out_width;
+        if (out && cap >= n) {
+            if (out_dev) {
+                CUDA_CHECK(cudaMemcpyAsync(out, out_d_.p, n * 4, cudaMemcpyDeviceToDevice, stream_));
+                CUDA_CHECK(cudaStreamSynchronize(stream_));
+            } else {
+                CUDA_CHECK(cudaMemcpyAsync(out, out_d_.p, n * 4, cudaMemcpyDeviceToHost, stream_));
+                CUDA_CHECK(cudaStreamSynchronize(stream_));
+            }
+        } else {
+            CUDA_CHECK(cudaStreamSynchronize(stream_));
+        }
+        CUDA_CHECK(cudaGetLastError());
+        finish_info(info);
+        prof_harvest();
+        return;
+    }
     const size_t fsz = (size_t)c * h * w;
     ensure_staging(c, h, w, true);
     // caller buffers are ordinary (pageable) host memory: stage through pinned
@@ -1061,6 +1127,10 @@ void Engine::run_frame(const float* frame, int c, int h, int w, const float* h9,
     }
     enqueue(frame_d_.p, c, h, w, h9, roi_dev);
     const size_t n = (size_t)pending_.out_channels * pending_.out_height * pending_.out_width;
+    if (out_dev && out && cap >= n) {
+        CUDA_CHECK(cudaMemcpyAsync(out, out_d_.p, n * 4, cudaMemcpyDeviceToDevice, stream_));
+        out = nullptr;
+    }
     const bool want = out && cap >= n;
     if (want) {
         if (out_h_n_ < n) {
@@ -1328,6 +1398,20 @@ int dfx_engine_create(const dfx_net_desc* net, const dfx_engine_config* cfg, int
     });
 }
 
+int dfx_engine_create_on_stream(const dfx_net_desc* net, const dfx_engine_config* cfg, int device, void* stream,
+                                dfx_engine** out) {
+    return guard([&] {
+        auto* h = new dfx_engine{nullptr};
+        try {
+            h->e = new Engine(net, cfg, device, static_cast<cudaStream_t>(stream));
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
 int dfx_engine_destroy(dfx_engine* e) {
     return guard([&] {
         if (!e) return;
@@ -1339,6 +1423,16 @@ int dfx_engine_destroy(dfx_engine* e) {
 int dfx_engine_run_frame(dfx_engine* e, const float* frame, int c, int h, int w, const float* h9, const float* roi,
                          dfx_frame_info* info, float* out, size_t out_cap) {
     return guard([&] { e->e->run_frame(frame, c, h, w, h9, roi, info, out, out_cap); });
+}
+int dfx_engine_run_frame_ex(dfx_engine* e, const float* frame, int c, int h, int w, int frame_is_device,
+                            const float* h9, const float* roi, dfx_frame_info* info, float* out, size_t out_cap,
+                            int out_is_device) {
+    return guard([&] {
+        e->e->run_frame(frame, c, h, w, h9, roi, info, out, out_cap, frame_is_device != 0, out_is_device != 0);
+    });
+}
+int dfx_engine_layer_order(dfx_engine* e, int* order, int cap, int* n) {
+    return guard([&] { e->e->layer_order(order, cap, n); });
 }
 int dfx_engine_submit_frame(dfx_engine* e, const float* frame_dev, int c, int h, int w, const float* h9) {
     return guard([&] { e->e->submit(frame_dev, c, h, w, h9); });

@@ -1373,16 +1373,7 @@ __global__ void k_densify(Ctx c, BufDev acc, BufDev trunc, float* __restrict__ o
 }  // namespace
 
 // ------------------------------------------------------------- launchers
-static int num_sms_cached() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+static int num_sms_cached() { return device_sm_count(); }
 static int persistent_grid(long long work) {
     const long long cap = (long long)num_sms_cached() * 8;
     long long g = (work + kThreads - 1) / kThreads;

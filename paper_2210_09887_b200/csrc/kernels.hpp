@@ -67,7 +67,9 @@ struct DenseOut {
     float* out;
     Readback rb;
 };
-bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
+// Returns the number of kernels launched (1 cooperative, 2 two-pass) or 0 when
+// the packet shape needs the generic launch_trunc_max / launch_trunc_apply.
+int launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
                            float thr, int relu, PktDev out, unsigned* gbar, const DenseOut* dz = nullptr,
                            bool* dz_done = nullptr, BufDev pf0 = BufDev{nullptr, 0, 0},
                            BufDev pf1 = BufDev{nullptr, 0, 0});  // pf0 / pf1: consumer state prefetched per fired tile
@@ -104,6 +106,9 @@ void launch_conv_exact(const Ctx& c, cudaStream_t s, PktDev in, const float* w, 
 void launch_conv_tc(const Ctx& c, cudaStream_t s, PktDev in, const float* wsplit, int cin, int cin_pad, int cout,
                     int cout_pad, int k, int st, int r, PktDev out, int out_halo_geom, const int* list,
                     const int* count, int max_targets, int num_sms, float* ws, int splits);
+// Kernel sizes the gathered-target tensor-core conv handles (k <= 7); larger
+// kernels take k_conv_exact.
+bool conv_tc_supported(int k);
 int conv_tc_splits(int max_targets, int cin_pad, int cout_pad, int k, int num_sms);
 size_t conv_tc_weight_floats(int cin_pad, int cout_pad, int k);
 void conv_tc_prepare_weights(const float* w, int cin, int cout, int k, int cin_pad, int cout_pad, float* out);

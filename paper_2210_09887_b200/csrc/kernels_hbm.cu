@@ -361,13 +361,14 @@ __device__ void commit_body(const Ctx& c, const FrameDev& F, const PktDev& in, B
 
 __global__ void __launch_bounds__(256) k_trunc_commit(Ctx c, PktDev in, BufDev acc, BufDev trunc,
                                                       const unsigned* __restrict__ tile_max, float thr, int relu,
-                                                      PktDev out) {
+                                                      PktDev out, BufDev pf0, BufDev pf1) {
     pdl_enter();
     __shared__ int s_list[kMaxList];
     __shared__ int s_warp[8];
     const FrameDev& F = *c.f;
     const int nl = build_tile_list(c, F, in, true, s_list, s_warp);
-    commit_body(c, F, in, acc, trunc, tile_max, thr, relu, out, s_list, nl);
+    commit_body(c, F, in, acc, trunc, tile_max, thr, relu, out, s_list, nl, false, pf0.d ? &pf0 : nullptr,
+                pf1.d ? &pf1 : nullptr);
 }
 
 // Both passes in ONE cooperative persistent launch (every CTA resident): the
@@ -547,15 +548,21 @@ __global__ void __launch_bounds__(256) k_maxpool_vec(Ctx c, PktDev in, BufDev ac
     }
 }
 
-// Persistent grid: SMs x resident CTAs per SM for this kernel.
+// Persistent grid: SMs x resident CTAs per SM for this kernel, on the calling
+// thread's current device (the carveout attribute and the SM count are per
+// device: `cache` is the call site's per-device memo).
 template <typename K>
-int stream_grid(K kernel) {
+int stream_grid(K kernel, std::atomic<int> (&cache)[64]) {
     int dev = 0, sms = 148, per = 1;
-    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaGetDevice(&dev);
+    const int hit = cache[dev & 63].load(std::memory_order_relaxed);
+    if (hit) return hit;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, 256, 0);
-    return sms * (per < 1 ? 1 : per);
+    const int g = sms * (per < 1 ? 1 : per);
+    cache[dev & 63].store(g, std::memory_order_relaxed);
+    return g;
 }
 
 }  // namespace
@@ -563,13 +570,14 @@ int stream_grid(K kernel) {
 static unsigned long long* g_trunc_trace = nullptr;
 unsigned long long* trunc_trace_buffer() { return g_trunc_trace; }
 
-bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
+int launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
                            float thr, int relu, PktDev out, unsigned* gbar, const DenseOut* dzp, bool* dz_done,
                            BufDev pf0, BufDev pf1) {
     if (dz_done) *dz_done = false;
     const DenseOut dz = (dzp && (acc.C & 7) == 0) ? *dzp : DenseOut{nullptr, Readback{}};
-    if ((in.C & 3) != 0) return false;
-    static const int gc = stream_grid(k_trunc_coop);
+    if ((in.C & 3) != 0) return 0;
+    static std::atomic<int> gc_cache[64];
+    const int gc = stream_grid(k_trunc_coop, gc_cache);
     // two launches by default: at the C2 ~10 % update rate the cooperative
     // single launch (co-residency wait, no programmatic overlap) measured
     // 1.5-2.5 % slower; DFX_TRUNC_COOP=1 selects it (it also hosts the output
@@ -605,19 +613,21 @@ bool launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, 
         if (cudaLaunchKernelEx(&cfg, k_trunc_coop, c, in, acc, trunc, tile_max, thr, relu, out, gbar, tr, 0, dz, pf0, pf1) ==
             cudaSuccess) {
             if (dz_done) *dz_done = dz.out != nullptr;
-            return true;
+            return 1;
         }
         cudaGetLastError();  // fall back to two launches
     }
-    static const int g1 = stream_grid(k_trunc_tilemax), g2 = stream_grid(k_trunc_commit);
+    static std::atomic<int> g1_cache[64], g2_cache[64];
+    const int g1 = stream_grid(k_trunc_tilemax, g1_cache), g2 = stream_grid(k_trunc_commit, g2_cache);
     launch_pdl(k_trunc_tilemax, g1, 256, 0, s, c, in, trunc, tile_max);
-    launch_pdl(k_trunc_commit, g2, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out);
-    return true;
+    launch_pdl(k_trunc_commit, g2, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out, pf0, pf1);
+    return 2;
 }
 
 bool launch_maxpool_vec(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, PktDev out) {
     if ((in.C & 3) != 0) return false;
-    static const int g = stream_grid(k_maxpool_vec);
+    static std::atomic<int> g_cache[64];
+    const int g = stream_grid(k_maxpool_vec, g_cache);
     launch_pdl(k_maxpool_vec, g, 256, 0, s, c, in, acc, prev, k, out);
     return true;
 }

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <stdlib.h>
 
+#include <atomic>
 #include <utility>
 
 namespace dfx {
@@ -49,6 +50,34 @@ inline bool pdl_enabled() {
         return (e && e[0] == '0') ? 0 : 1;
     }();
     return on != 0;
+}
+
+// One-time setup per device (kernel attributes belong to a device context, so
+// an engine on a second GPU of the same process needs its own): runs f() once
+// for the calling thread's current device. Concurrent first calls may both run
+// f(); the setups used here are idempotent.
+template <typename F>
+inline void once_per_device(std::atomic<unsigned long long>& done, F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    f();
+    done.fetch_or(bit, std::memory_order_acq_rel);
+}
+
+// SM count of the calling thread's current device (cached per device).
+inline int device_sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int n = cache[dev & 63].load(std::memory_order_relaxed);
+    if (!n) {
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+        cache[dev & 63].store(n, std::memory_order_relaxed);
+    }
+    return n;
 }
 
 template <typename... KArgs, typename... Args>

@@ -255,3 +255,137 @@ def vgg8_net(rng=None, in_channels=3, widths=(64, 64, "P", 128, 128, "P", 256, 2
         ch = wdt
     spec.output(cur)
     return spec
+
+
+def _he_conv(spec, rng, name, inp, cin, cout, k, stride=1, bias=True):
+    lim = float(np.sqrt(6.0 / (cin * k * k)))
+    w = rng.uniform(-lim, lim, size=(cout, cin, k, k)).astype(np.float32)
+    b = rng.uniform(-0.05, 0.05, size=cout).astype(np.float32) if bias else None
+    return spec.conv(name, inp, w, b, stride)
+
+
+def resnet18_net(rng=None, in_channels=3, widths=(64, 128, 256, 512)):
+    """ResNet-18-style delta backbone. 7x7 stride-2 stem +
+    relu, 2x2 max pool (the engine requires k == stride, network.cpp:164-166),
+    four stages of two basic blocks (conv3x3(s) -> relu -> conv3x3 -> add
+    shortcut -> relu); the first block of stages 2-4 is strided with a 1x1
+    stride-2 projection shortcut. BN folded into the conv biases. He-uniform
+    random weights. Tile 32 gives per-layer tiles 16 (stem), 8, 4, 2, 1."""
+    rng = rng or np.random.default_rng(2210)
+    spec = NetworkSpec(in_channels=in_channels)
+    cur = _he_conv(spec, rng, "stem", "input", in_channels, widths[0], 7, 2)
+    cur = spec.relu("stem_relu", cur)
+    cur = spec.maxpool("pool", cur)
+    ch = widths[0]
+    for si, wd in enumerate(widths):
+        for bi in range(2):
+            p = f"s{si + 1}b{bi + 1}"
+            stride = 2 if (si > 0 and bi == 0) else 1
+            c1 = _he_conv(spec, rng, p + "_conv1", cur, ch, wd, 3, stride)
+            r1 = spec.relu(p + "_relu1", c1)
+            c2 = _he_conv(spec, rng, p + "_conv2", r1, wd, wd, 3, 1)
+            sc = cur
+            if stride != 1 or ch != wd:
+                sc = _he_conv(spec, rng, p + "_proj", cur, ch, wd, 1, stride)
+            a = spec.add(p + "_add", c2, sc)
+            cur = spec.relu(p + "_relu2", a)
+            ch = wd
+    spec.output(cur)
+    return spec
+
+
+def hrnet_w32_net(rng=None, in_channels=3, widths=(32, 64, 128, 256), joints=17):
+    """HRNet-W32-style pose network. Stem of two 3x3 stride-2
+    convs (stride 4), then branches of 32 / 64 / 128 / 256 channels at stride
+    4 / 8 / 16 / 32 added one per stage by a 3x3 stride-2 transition conv; each
+    stage runs one basic block per branch and fuses every branch into the
+    higher-resolution ones by 1x1 conv + nearest upsample + add and into the
+    lower-resolution ones by 3x3 stride-2 convs + add; a 1x1 head gives
+    `joints` heatmaps at stride 4. With tile 32 the stride-32 branch has 1-px
+    tiles (network.cpp:113-119)."""
+    rng = rng or np.random.default_rng(2210)
+    spec = NetworkSpec(in_channels=in_channels)
+    n = [0]
+
+    def nm(base):
+        n[0] += 1
+        return f"{base}{n[0]}"
+
+    def conv(inp, cin, cout, k, s=1):
+        return _he_conv(spec, rng, nm("conv"), inp, cin, cout, k, s)
+
+    def relu(inp):
+        return spec.relu(nm("relu"), inp)
+
+    x = relu(conv("input", in_channels, 64, 3, 2))
+    x = relu(conv(x, 64, 64, 3, 2))
+    branches = [relu(conv(x, 64, widths[0], 3))]
+    for stage in range(1, len(widths) + 1):
+        # one basic block per branch
+        nb = []
+        for b, cur in enumerate(branches):
+            c = widths[b]
+            y = relu(conv(cur, c, c, 3))
+            y = conv(y, c, c, 3)
+            nb.append(relu(spec.add(nm("add"), y, cur)))
+        branches = nb
+        if stage == len(widths):
+            break
+        # fusion: every branch receives the others (up: 1x1 + upsample; down: 3x3 s2 chain)
+        fused = []
+        for i in range(len(branches)):
+            acc = branches[i]
+            for j in range(len(branches)):
+                if j == i:
+                    continue
+                if j > i:
+                    y = conv(branches[j], widths[j], widths[i], 1)
+                    y = spec.upsample(nm("up"), y, factor=2 ** (j - i))
+                else:
+                    y = branches[j]
+                    cj = widths[j]
+                    for step in range(i - j):
+                        co = widths[i] if step == i - j - 1 else cj
+                        y = conv(y, cj, co, 3, 2)
+                        if step != i - j - 1:
+                            y = relu(y)
+                        cj = co
+                acc = spec.add(nm("add"), acc, y)
+            fused.append(relu(acc))
+        # transition: a new lower-resolution branch from the last one
+        fused.append(relu(conv(fused[-1], widths[len(branches) - 1], widths[len(branches)], 3, 2)))
+        branches = fused
+    # final fusion of every branch into the stride-4 one, then the heatmap head
+    acc = branches[0]
+    for j in range(1, len(branches)):
+        y = spec.upsample(nm("up"), conv(branches[j], widths[j], widths[0], 1), factor=2 ** j)
+        acc = spec.add(nm("add"), acc, y)
+    head = conv(relu(acc), widths[0], joints, 1)
+    spec.output(spec.truncate("head_trunc", head))
+    return spec
+
+
+def patch_update_sequence(rng, c, h, w, frames, frac, tile, pan_x=0, pan_y=0):
+    """SURVEY §8(d) C4 update-rate sweep: a static textured scene seen through
+    an integer-translation camera (pan_x, pan_y px/frame); every frame a
+    fraction `frac` of the frame's tiles (tile-aligned in world coordinates)
+    receives a new textured patch, so the input update rate is ~frac."""
+    sx, sy = abs(pan_x) * (frames - 1), abs(pan_y) * (frames - 1)
+    world = texture(rng, c, h + sy + tile, w + sx + tile)
+    patches = texture(rng, c, tile * 8, tile * 8)
+    out = []
+    for f in range(frames):
+        wx = pan_x * f if pan_x >= 0 else sx + pan_x * f
+        wy = pan_y * f if pan_y >= 0 else sy + pan_y * f
+        if f > 0 and frac > 0:
+            ty0, tx0 = -(-wy // tile), -(-wx // tile)
+            nty, ntx = (h - (ty0 * tile - wy)) // tile, (w - (tx0 * tile - wx)) // tile
+            cells = nty * ntx
+            pick = rng.choice(cells, size=max(1, int(round(frac * cells))), replace=False)
+            for p in pick:
+                y = (ty0 + p // ntx) * tile
+                x = (tx0 + p % ntx) * tile
+                py, px = rng.integers(0, 7) * tile, rng.integers(0, 7) * tile
+                world[:, y:y + tile, x:x + tile] = patches[:, py:py + tile, px:px + tile]
+        out.append((np.ascontiguousarray(world[:, wy:wy + h, wx:wx + w]), translation(wx, wy)))
+    return out

@@ -63,3 +63,23 @@ def test_gloo_world2_partition_and_reductions():
         assert sorted(flat) == list(range(64)) and len(set(flat)) == 64
         assert total == 640
         assert slowest == 2.0
+
+
+def test_bench_gpus_2_spawns_two_ranks():
+    """`python bench.py --gpus 2` without a torchrun environment launches two
+    ranks itself (one process per GPU; gloo in the dry run) and rank 0 prints
+    the job line with n_gpus = 2 and the max-over-ranks time."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["ms_max"] == 11.0
+    assert d["streams_per_rank"] == [[0], [1]]
