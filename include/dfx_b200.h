@@ -24,7 +24,17 @@
  *   dfx_engine_read_packet   the per-layer DeltaPacket the observer sees  engine.hpp:69-70, engine.cpp:239,279
  *   dfx_engine_read_ledger   DeltaEngine::ledger()                     engine.hpp:64 (TileLedger, buffer_manager.hpp:13-88)
  *   dfx_wrap_tile            dflx::wrap_tile                            tile_grid.hpp:37-40
+ *   dfx_validate_net         dflx::validate (host only)                 network.hpp:61-65, network.cpp:46-254
  *   dfx_ledger_*             dflx::TileLedger + plan_frame + apply_plan buffer_manager.hpp:13-126
+ *   dfx_layer_ctx_*          one frame's FramePlacement + slot filter     tile_grid.hpp:43-58, delta_layers.hpp:50-57
+ *   dfx_input_stage          compute_input_delta + DeltaEngine::input_gate + the gated input truncation
+ *                            alignment.cpp:168-192, engine.cpp:110-182, 233-237
+ *   dfx_claim_reset          apply_plan + zero_tile_everywhere + inject_bias_implicit
+ *                            buffer_manager.cpp:68-89, engine.cpp:78-91
+ *   dfx_delta_conv           dflx::padded_delta_conv                    delta_layers.hpp:103-104, delta_layers.cpp:100-147
+ *   dfx_delta_truncate       dflx::delta_activation_truncate            delta_layers.hpp:114-116, delta_layers.cpp:149-232
+ *   dfx_delta_maxpool        dflx::delta_maxpool                        delta_layers.hpp:118-119, delta_layers.cpp:234-318
+ *   dfx_densify              dflx::densify                              delta_layers.hpp:127, delta_layers.cpp:395-400
  *
  * Conventions: every call returns 0 on success and a nonzero dfx_status on
  * failure; dfx_last_error() returns a thread-local message (C++ exceptions
@@ -247,6 +257,11 @@ int dfx_engine_timer_stop(dfx_engine* e, float* ms);
 
 void dfx_wrap_tile(int64_t tx, int64_t ty, int rows, int cols, int* row, int* col);
 
+/* Host-only network validation (dflx::validate, network.cpp:46-254): the
+ * checks dfx_engine_create runs, without a device. On success `topo` holds
+ * the execution order (*n entries) and *ring the stash ring width in tiles. */
+int dfx_validate_net(const dfx_net_desc* net, int tile_size, int* topo, int cap, int* n, int* ring);
+
 /* Host-only tile ledger: the TileLedger / plan_frame / apply_plan the engine
  * plans every frame with (buffer_manager.hpp:13-126, buffer_manager.cpp:7-81;
  * full reset + replan as engine.cpp:207-211). dfx_ledger_step plans and
@@ -260,6 +275,95 @@ int dfx_ledger_step(dfx_ledger* h, int64_t otx, int64_t oty, int th, int tw, int
                     int64_t* claims, int* victims, size_t claim_cap, int* nclaims, int64_t* fresh, size_t fresh_cap,
                     int* nfresh, int* evicted);
 int dfx_ledger_slots(dfx_ledger* h, int* used, int64_t* ty, int64_t* tx, uint8_t* covered, size_t cap);
+
+/* ===================================================================== layer level
+ * The reference's layer functions (delta_layers.hpp:103-127), used directly by
+ * its unit tests, on DEVICE buffers in this library's native layouts:
+ *
+ *   dfx_packet (DeltaPacket, delta_layers.hpp:18-46): `d` = dense grown extent,
+ *     HWC, (rows*tile + 2*halo) x (cols*tile + 2*halo) x channels floats (the
+ *     grid's rows / cols, not the placement's); `ext` = tile validity bytes
+ *     over (rows + 2*RT) x (cols + 2*RT) tiles, RT = ceil(halo / tile): inside
+ *     the placement it IS the TileMask, ring tiles flag written halo data.
+ *   dfx_state (SphericalBuffer, tile_grid.hpp:88-128): slot-major
+ *     [rows][cols][tile][tile][channels] floats.
+ *
+ * A dfx_layer_ctx binds one device, one cudaStream_t and one grid; its frame
+ * (dfx_layer_ctx_set_frame) is the placement plus the slot table the slot
+ * filter reads (TileLedger::holds, buffer_manager.hpp:41-44). Calls are
+ * stream-ordered and asynchronous except where they return host values.
+ * dfx_packet_from_chw / _to_chw and dfx_state_from_chw / _to_chw convert
+ * from / to the reference's layouts (dense grown CHW + TileMask; wrapped CHW
+ * planar), device to device. */
+typedef struct dfx_layer_ctx dfx_layer_ctx;
+typedef struct {
+    int64_t origin_tx, origin_ty; /* FramePlacement::origin (tiles) */
+    int tiles_h, tiles_w;
+} dfx_placement;
+typedef struct {
+    int used;
+    int64_t tx, ty; /* the global tile the slot holds */
+} dfx_slot;
+typedef struct {
+    float* d;
+    uint8_t* ext;
+    int channels, tile, halo;
+} dfx_packet;
+typedef struct {
+    float* d;
+    int channels, tile;
+} dfx_state;
+
+int dfx_layer_ctx_create(int rows, int cols, int device, void* stream, dfx_layer_ctx** out);
+int dfx_layer_ctx_destroy(dfx_layer_ctx* c);
+/* slots: rows*cols host entries in row-major (floor_mod(ty, rows), floor_mod(tx,
+ * cols)) order, or NULL = every slot holds the placement tile that maps to it. */
+int dfx_layer_ctx_set_frame(dfx_layer_ctx* c, const dfx_placement* place, const dfx_slot* slots);
+/* Device buffer sizes of a packet / state on this grid. */
+size_t dfx_packet_floats(const dfx_layer_ctx* c, int channels, int tile, int halo);
+size_t dfx_packet_ext_bytes(const dfx_layer_ctx* c, int tile, int halo);
+size_t dfx_state_floats(const dfx_layer_ctx* c, int channels, int tile);
+/* chw: device, channels x (th*tile + 2*halo) x (tw*tile + 2*halo); mask: host th*tw bytes. */
+int dfx_packet_from_chw(dfx_layer_ctx* c, const float* chw, const uint8_t* mask, dfx_packet* out);
+int dfx_packet_to_chw(dfx_layer_ctx* c, const dfx_packet* p, float* chw, uint8_t* mask);
+/* chw: device, channels x (rows*tile) x (cols*tile), the reference's wrapped planar layout. */
+int dfx_state_from_chw(dfx_layer_ctx* c, const float* chw, dfx_state* out);
+int dfx_state_to_chw(dfx_layer_ctx* c, const dfx_state* s, float* chw);
+
+/* padded_delta_conv: out halo = windowed_out_halo(in halo, k, k/2, stride),
+ * out tile = in tile / stride (dfx_delta_conv_out_halo); weights: device
+ * O-I-K-K fp32 (bias is never applied here, delta_layers.hpp:100-102);
+ * conv_mode DFX_CONV_TF32X3 or DFX_CONV_EXACT. *flops (host, may be NULL)
+ * receives the reference's FlopReport counts (flops, dense_flops). */
+int dfx_delta_conv_out_halo(int in_halo, int kernel, int stride);
+int dfx_delta_conv(dfx_layer_ctx* c, const dfx_packet* in, const float* weights, int cin, int cout, int kernel,
+                   int stride, int conv_mode, dfx_packet* out, uint64_t* flops);
+/* delta_activation_truncate (no gate: the input stage's gate is dfx_input_stage);
+ * relu = 1 for ActKind::Relu, 0 for Identity. Out packet: halo 0, in tile. */
+int dfx_delta_truncate(dfx_layer_ctx* c, const dfx_packet* in, dfx_state* acc, dfx_state* trunc, float threshold,
+                       int relu, dfx_packet* out);
+/* delta_maxpool (k == stride): acc at the input tile, prev at the output tile;
+ * out halo = windowed_out_halo(in halo, k, 0, k). */
+int dfx_delta_maxpool(dfx_layer_ctx* c, const dfx_packet* in, dfx_state* acc, dfx_state* prev, int k,
+                      dfx_packet* out);
+/* densify: out (device, CHW channels x th*tile x tw*tile) = acc + trunc. */
+int dfx_densify(dfx_layer_ctx* c, const dfx_state* acc, const dfx_state* trunc, float* out);
+/* Claim reset: every claimed tile (coords: host (tx, ty) pairs) is zeroed in
+ * every state, then filled with fills[b] (per-channel, device, or NULL = 0)
+ * for states with a bias init (apply_plan + inject_bias_implicit). */
+int dfx_claim_reset(dfx_layer_ctx* c, const int64_t* coords, int nclaims, dfx_state* const* states,
+                    const float* const* fills, int nstates);
+/* Input stage on an ALIGNED frame (the canvas of alignment.cpp:106-166):
+ * aligned: device CHW channels x (th*T) x (tw*T); valid: device bytes (th*T) x
+ * (tw*T), 1 where the pixel came from the frame; roi_factor: device floats
+ * (th*T) x (tw*T) or NULL; fresh: host th*tw bytes or NULL. Computes
+ * raw = aligned - acc on covered tiles, the gate (significance > threshold,
+ * noise rule, dilation, fresh tiles) and the gated truncation into
+ * acc / trunc; `out` (halo 0) receives the fired candidates and the gate as
+ * mask; *update_rate (host, may be NULL) = fired tiles / placement tiles. */
+int dfx_input_stage(dfx_layer_ctx* c, const float* aligned, const uint8_t* valid, const float* roi_factor,
+                    const uint8_t* fresh, float threshold, int dilation, int noise_suppression, dfx_state* acc,
+                    dfx_state* trunc, dfx_packet* out, double* update_rate);
 
 #ifdef __cplusplus
 }

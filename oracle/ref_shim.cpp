@@ -435,3 +435,146 @@ int dfr_ledger_slots(void* hv, int* used, int64_t* ty, int64_t* tx, uint8_t* cov
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- layer level
+// The reference's free layer functions (delta_layers.hpp:103-127) on host
+// buffers in its own layouts, for tests/test_gpu_layers.py: packets as dense
+// grown CHW + TileMask bytes, states as wrapped CHW planar storage, the slot
+// filter from a rows*cols dfx_slot table (TileLedger::holds semantics).
+namespace {
+
+DeltaPacket packet_from(const dfx_placement* pl, int tile, int halo, int C, const float* chw, const uint8_t* mask) {
+    FramePlacement p;
+    p.origin = TileCoord{pl->origin_tx, pl->origin_ty};
+    p.tiles_h = pl->tiles_h;
+    p.tiles_w = pl->tiles_w;
+    DeltaPacket k = make_packet(p, tile, tile, C, halo);
+    std::memcpy(k.delta.data.data(), chw, k.delta.size() * sizeof(float));
+    for (size_t i = 0; i < k.mask.bits.size(); ++i) k.mask.bits[i] = mask[i] ? 1 : 0;
+    return k;
+}
+
+void packet_to(const DeltaPacket& k, float* chw, uint8_t* mask, int* halo) {
+    std::memcpy(chw, k.delta.data.data(), k.delta.size() * sizeof(float));
+    for (size_t i = 0; i < k.mask.bits.size(); ++i) mask[i] = k.mask.bits[i];
+    if (halo) *halo = k.halo;
+}
+
+SphericalBuffer buffer_from(int rows, int cols, int tile, int C, const float* chw) {
+    SphericalBuffer b(GridSpec{tile, tile, rows, cols}, C);
+    const int PH = rows * tile, PW = cols * tile;
+    for (int c = 0; c < C; ++c)
+        for (int y = 0; y < PH; ++y)
+            for (int x = 0; x < PW; ++x) b.at_global(c, y, x) = chw[((size_t)c * PH + y) * PW + x];
+    return b;
+}
+
+void buffer_to(const SphericalBuffer& b, float* chw) {
+    std::memcpy(chw, b.storage().data(), b.storage().size() * sizeof(float));
+}
+
+SlotFilter filter_from(const dfx_slot* slots, int rows, int cols) {
+    if (!slots) return {};
+    std::vector<dfx_slot> s(slots, slots + (size_t)rows * cols);
+    return [s, rows, cols](const TileCoord& t) {
+        const dfx_slot& q = s[(size_t)floor_mod(t.ty, rows) * cols + floor_mod(t.tx, cols)];
+        return q.used && q.tx == t.tx && q.ty == t.ty;
+    };
+}
+
+}  // namespace
+
+extern "C" {
+
+int dfr_layer_conv(const dfx_placement* pl, int tile, int halo, int C, const float* chw, const uint8_t* mask,
+                   const float* w, int cout, int k, int stride, float* out_chw, uint8_t* out_mask, int* out_halo,
+                   uint64_t* flops) {
+    try {
+        const DeltaPacket in = packet_from(pl, tile, halo, C, chw, mask);
+        ConvParams p;
+        p.in_channels = C;
+        p.out_channels = cout;
+        p.kernel_h = p.kernel_w = k;
+        p.stride = stride;
+        p.padding = k / 2;
+        p.weights.assign(w, w + (size_t)cout * C * k * k);
+        FlopReport fr;
+        const DeltaPacket out = padded_delta_conv(in, p, &fr, "conv");
+        packet_to(out, out_chw, out_mask, out_halo);
+        flops[0] = fr.total;
+        flops[1] = fr.dense_total;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_with(e);
+    }
+}
+
+int dfr_layer_truncate(const dfx_placement* pl, int rows, int cols, int tile, int halo, int C, const float* chw,
+                       const uint8_t* mask, float* acc, float* trunc, float thr, int relu, const dfx_slot* slots,
+                       float* out_chw, uint8_t* out_mask) {
+    try {
+        const DeltaPacket in = packet_from(pl, tile, halo, C, chw, mask);
+        TruncationState st(GridSpec{tile, tile, rows, cols}, C, thr);
+        st.accumulated = buffer_from(rows, cols, tile, C, acc);
+        st.truncated = buffer_from(rows, cols, tile, C, trunc);
+        const DeltaPacket out = delta_activation_truncate(in, st, relu ? ActKind::Relu : ActKind::Identity,
+                                                          filter_from(slots, rows, cols));
+        packet_to(out, out_chw, out_mask, nullptr);
+        buffer_to(st.accumulated, acc);
+        buffer_to(st.truncated, trunc);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_with(e);
+    }
+}
+
+int dfr_layer_maxpool(const dfx_placement* pl, int rows, int cols, int tile, int halo, int C, const float* chw,
+                      const uint8_t* mask, float* acc, float* prev, int k, const dfx_slot* slots, float* out_chw,
+                      uint8_t* out_mask, int* out_halo) {
+    try {
+        const DeltaPacket in = packet_from(pl, tile, halo, C, chw, mask);
+        MaxPoolState st(GridSpec{tile, tile, rows, cols}, GridSpec{tile / k, tile / k, rows, cols}, C, k, k, 0);
+        st.accumulated = buffer_from(rows, cols, tile, C, acc);
+        st.prev_out = buffer_from(rows, cols, tile / k, C, prev);
+        const DeltaPacket out = delta_maxpool(in, st, filter_from(slots, rows, cols));
+        packet_to(out, out_chw, out_mask, out_halo);
+        buffer_to(st.accumulated, acc);
+        buffer_to(st.prev_out, prev);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_with(e);
+    }
+}
+
+int dfr_layer_densify(const dfx_placement* pl, int rows, int cols, int tile, int C, const float* acc,
+                      const float* trunc, float* out) {
+    try {
+        TruncationState st(GridSpec{tile, tile, rows, cols}, C, 0.0f);
+        st.accumulated = buffer_from(rows, cols, tile, C, acc);
+        st.truncated = buffer_from(rows, cols, tile, C, trunc);
+        FramePlacement p;
+        p.origin = TileCoord{pl->origin_tx, pl->origin_ty};
+        p.tiles_h = pl->tiles_h;
+        p.tiles_w = pl->tiles_w;
+        const Tensor t = densify(st, p);
+        std::memcpy(out, t.data.data(), t.size() * sizeof(float));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_with(e);
+    }
+}
+
+}  // extern "C"
+
+extern "C" {
+// dflx::save_network (network.cpp:425-500): JSON + one DFLX file per weight
+// tensor (the reference's on-disk format), for the loader tests.
+int dfr_save_network(const dfx_net_desc* net, const char* path) {
+    try {
+        save_network(spec_from(net), path);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_with(e);
+    }
+}
+}  // extern "C"

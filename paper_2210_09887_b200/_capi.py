@@ -189,6 +189,10 @@ def load_library():
         fn.restype = res
         fn.argtypes = args
         api[name] = fn
+    fn = lib.dfx_validate_net
+    fn.restype = C.c_int
+    fn.argtypes = [C.POINTER(NetDesc), C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    api["validate_net"] = fn
     fn = lib.dfx_host_alloc
     fn.restype = C.c_void_p
     fn.argtypes = [C.c_size_t]

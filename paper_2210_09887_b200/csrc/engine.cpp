@@ -1351,6 +1351,11 @@ struct dfx_engine {
 
 namespace {
 thread_local std::string g_last;
+}  // namespace
+namespace dfx {
+void set_last_error(const std::string& m) { g_last = m; }
+}  // namespace dfx
+namespace {
 template <typename F>
 int guard(F&& f) {
     try {
@@ -1617,6 +1622,17 @@ int dfx_engine_timer_start(dfx_engine* e) {
 }
 int dfx_engine_timer_stop(dfx_engine* e, float* ms) {
     return guard([&] { *ms = e->e->timer_stop(); });
+}
+
+int dfx_validate_net(const dfx_net_desc* net, int tile_size, int* topo, int cap, int* n, int* ring) {
+    return guard([&] {
+        const dfx::Net v = dfx::validate_net(net, tile_size);
+        int k = 0;
+        for (int i : v.topo)
+            if (k < cap) topo[k++] = i;
+        *n = k;
+        if (ring) *ring = v.ring;
+    });
 }
 
 void dfx_wrap_tile(int64_t tx, int64_t ty, int rows, int cols, int* row, int* col) {

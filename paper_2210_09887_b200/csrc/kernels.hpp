@@ -168,3 +168,11 @@ void launch_frame_begin(cudaStream_t s, const void* src, void* dst, size_t bytes
 void launch_set_flag(cudaStream_t s, unsigned* f, unsigned v);
 
 }  // namespace dfx
+
+namespace dfx {
+// ---- layout conversions for the layer-level C-ABI (layout.cu) ----
+void launch_pkt_from_chw(cudaStream_t s, const float* chw, const uint8_t* mask_dev, int th, int tw, PktDev p);
+void launch_pkt_to_chw(cudaStream_t s, PktDev p, int th, int tw, float* chw, uint8_t* mask_dev);
+void launch_state_convert(cudaStream_t s, const float* src, float* dst, int C, int t, int rows, int cols, int to_chw);
+void launch_canvas_from_chw(cudaStream_t s, const float* chw, int C, int h, int w, float* canvas, int pitch);
+}  // namespace dfx

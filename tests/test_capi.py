@@ -12,6 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "dfx_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)  # declarations only, not comments
     return sorted(set(re.findall(r"\b(dfx_[a-z_]+)\s*\(", src)))
 
 
