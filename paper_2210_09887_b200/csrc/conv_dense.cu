@@ -129,10 +129,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+template <bool TM>
 __global__ void __launch_bounds__(kPlanThreads) k_conv_plan(Ctx c, PlanArgs pa) {
     pdl_enter();
     __shared__ PlanSmem sm;
-    plan_block<kPlanThreads>(c, pa, blockIdx.x, sm);
+    plan_block<kPlanThreads, TM>(c, pa, blockIdx.x, sm);
 }
 
 struct DenseArgs {
@@ -155,6 +156,8 @@ struct DenseArgs {
     int npb;               // patch ring depth (raw fp32 patches; the producers split hi / lo)
     int nmma;              // MMA issuer warps (2: K-block pairs alternate, one accumulator each)
     BufDev nxt_acc, nxt_trunc;  // the consuming activation's state (L2 prefetch of this CTA's tiles), .d = null: none
+    unsigned* tmax;        // fused tile max (pass 1 of the consuming activation): max |trunc + delta| per
+                           // placement tile, atomicMax on the float bits; null: the activation computes it
     long long* trace;      // microbenchmark (dbg & 64): per-K-block clock64 stamps of CTA 0
     int dbg;               // microbenchmark knobs (tools/bench_conv.cu): 1 no MMA, 2 no patch, 4 no weights
 };
@@ -184,6 +187,36 @@ __device__ __forceinline__ bool unit_pixel(const DenseArgs& a, int listed, int u
     y = (((tv >> 16) - 8) << a.tsh) + (l >> a.tsh);
     x = (((tv & 0xffff) - 8) << a.tsh) + (l & ((1 << a.tsh) - 1));
     return true;
+}
+
+// Fused pass 1 of the consuming activation (delta_layers.cpp:194-201):
+// max |trunc + delta| over channels [o0, o0 + 4*n4) of placement pixel (y, x)
+// of the activation's truncated state (slot-major, channels innermost).
+template <int N4>
+__device__ __forceinline__ float trunc_amax(const Ctx& c, const FrameDev& F, const BufDev& tr, int y, int x, int o0,
+                                            const float* v) {
+    const int t = tr.t, qy = y / t, qx = x / t;
+    const float4* p = reinterpret_cast<const float4*>(tr.d + (size_t)slot_of(F, c.rows, c.cols, qy, qx) * t * t * tr.C +
+                                                      ((size_t)(y - qy * t) * t + (x - qx * t)) * tr.C + o0);
+    float4 tv[N4];
+#pragma unroll
+    for (int k4 = 0; k4 < N4; ++k4) tv[k4] = __ldcg(p + k4);  // all loads in flight first
+    float m = 0.0f;
+#pragma unroll
+    for (int k4 = 0; k4 < N4; ++k4) {
+        m = fmaxf(m, fabsf(__fadd_rn(tv[k4].x, v[4 * k4])));
+        m = fmaxf(m, fabsf(__fadd_rn(tv[k4].y, v[4 * k4 + 1])));
+        m = fmaxf(m, fabsf(__fadd_rn(tv[k4].z, v[4 * k4 + 2])));
+        m = fmaxf(m, fabsf(__fadd_rn(tv[k4].w, v[4 * k4 + 3])));
+    }
+    return m;
+}
+// Lanes with the same tile key (-1: none) reduce their maxima (non-negative
+// floats order as their bits) and the group leader folds it into tile_max.
+__device__ __forceinline__ void tile_max_fold(unsigned* tmax, unsigned lanes, int key, float m) {
+    const unsigned grp = __match_any_sync(lanes, key);
+    const unsigned mx = __reduce_max_sync(grp, __float_as_uint(m));
+    if (key >= 0 && mx != 0u && (threadIdx.x & 31) == (unsigned)(__ffs(grp) - 1)) atomicMax(tmax + key, mx);
 }
 
 struct DenseSched {
@@ -762,13 +795,18 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
         const int nq = (o1 - o0 + 3) / 4;  // float4 columns per row
         const size_t sstride = (size_t)n * 128 * a.cout_pad;
         const bool vec = (a.out.C & 3) == 0;
-        for (int e = tid; e < nu * nm * nq; e += blockDim.x) {
+        const int ntot = nu * nm * nq;
+        for (int e0 = tid & ~31; e0 < ntot; e0 += blockDim.x) {  // warp-uniform trip count (tile max fold)
+            const int e = e0 + lane;
             const int j = e / (nm * nq), rem = e - j * nm * nq;
             const int m = m0 + rem / nq, c4 = rem - (rem / nq) * nq;
             const int u = UPI * pr + j;
-            int y, x;
-            if (!unit_pixel(a, listed, u, m, y, x)) continue;
-            if (!(y >= -hs && y < eh && x >= -hs && x < ew)) continue;
+            int y = 0, x = 0;
+            const bool live = e < ntot && unit_pixel(a, listed, u, m, y, x) && y >= -hs && y < eh && x >= -hs && x < ew;
+            if (!live) {
+                if (a.tmax) tile_max_fold(a.tmax, 0xffffffffu, -1, 0.0f);
+                continue;
+            }
             const int o = o0 + 4 * c4;
             const float* src = a.ws + ((size_t)u * 128 + m) * a.cout_pad + o;
             float4 v[8];
@@ -789,8 +827,49 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                 const float vv[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
                 for (int q = 0; q < 4 && o + q < o1; ++q) dst[q] = vv[q];
             }
+            if (a.tmax) {  // fused activation pass 1 on the final sums
+                const bool in_ext = y >= 0 && y < F.th * a.out.t && x >= 0 && x < F.tw * a.out.t && o + 4 <= o1;
+                const float vv[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
+                const float m4 = in_ext ? trunc_amax<1>(c, F, a.nxt_trunc, y, x, o, vv) : 0.0f;
+                tile_max_fold(a.tmax, 0xffffffffu, in_ext ? (y / a.out.t) * F.tw + x / a.out.t : -1, m4);
+            }
         }
         if (tid == 0) a.cnt[it / S] = 0;  // re-arm for the next frame
+    }
+    if (a.tmax && S == 1) {
+        // fused pass 1 of the consuming activation (delta_layers.cpp:194-201) over
+        // this CTA's items, by ALL threads once the items are done (the epilogue
+        // warps alone keep too few loads in flight, and in-loop work would hold up
+        // the next item): max |trunc + delta| per placement tile from the delta
+        // just stored by this CTA and the activation's truncated state
+        const int np = a.NBD / 32;  // 32-channel parts per pixel: one thread, 8 + 8 float4 loads in flight
+        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            int pr, nb, kb0, kb1;
+            item_info(it, pr, nb, kb0, kb1);
+            const int nu = (UPI == 2 && 2 * pr + 1 < n) ? 2 : 1;
+            const int ntot = nu * 128 * np;
+            for (int e0 = tid & ~31; e0 < ntot; e0 += blockDim.x) {  // warp-uniform trip count
+                const int e = e0 + lane;
+                const int j = e / (128 * np), rem = e - j * 128 * np;
+                const int m = rem / np, part = rem - m * np;
+                int y = 0, x = 0;
+                const bool in_ext = e < ntot && unit_pixel(a, listed, UPI * pr + j, m, y, x) && y >= 0 &&
+                                    y < F.th * a.out.t && x >= 0 && x < F.tw * a.out.t;
+                float mt = 0.0f;
+                if (in_ext) {
+                    const int o = nb * a.NBD + 32 * part;
+                    const float4* d4 = reinterpret_cast<const float4*>(a.out.d + pkt_off(a.out, y, x) + o);
+                    float v[32];
+#pragma unroll
+                    for (int k4 = 0; k4 < 8; ++k4) {
+                        const float4 q4 = __ldcg(d4 + k4);
+                        v[4 * k4] = q4.x, v[4 * k4 + 1] = q4.y, v[4 * k4 + 2] = q4.z, v[4 * k4 + 3] = q4.w;
+                    }
+                    mt = trunc_amax<8>(c, F, a.nxt_trunc, y, x, o, v);
+                }
+                tile_max_fold(a.tmax, 0xffffffffu, in_ext ? (y / a.out.t) * F.tw + x / a.out.t : -1, mt);
+            }
+        }
     }
     if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) a.trace[501] = clock64();
     if ((a.dbg & 64) && tid == 0 && blockIdx.x < 400) {
@@ -983,11 +1062,15 @@ void dense_conv_prepare_weights(const DenseConvPlan& p, const float* w, int cin,
 }
 
 void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, int hg, int* units,
-                      int* nunits, unsigned long long* flop_px, int tau, int* list, int* lcount) {
+                      int* nunits, unsigned long long* flop_px, int tau, int* list, int* lcount, unsigned* tmax,
+                      BufDev tm_trunc) {
     if (hg > 8) throw std::runtime_error("conv_plan: grown halo > 8 px");
     if (p.tpu && out.RT >= 8) throw std::runtime_error("conv_plan: tile ring too wide for tile units");
-    const PlanArgs pa{in, out, p.k, p.r, hg, p.nbw, p.nbh * p.nbw, units, nunits, flop_px, tau, list, lcount, p.tpu ? 1 : 0};
-    launch_pdl(k_conv_plan, p.nbh * p.nbw, kPlanThreads, 0, s, c, pa);
+    const PlanArgs pa{in,   out,  p.k,    p.r,    hg,          p.nbw, p.nbh * p.nbw, units, nunits,
+                      flop_px, tau, list, lcount, p.tpu ? 1 : 0, tmax,  tm_trunc};
+    // the zero-fill tile max exists only for 16x8-px units (tile units leave no zero fill)
+    if (tmax && !p.tpu) launch_pdl(k_conv_plan<true>, p.nbh * p.nbw, kPlanThreads, 0, s, c, pa);
+    else launch_pdl(k_conv_plan<false>, p.nbh * p.nbw, kPlanThreads, 0, s, c, pa);
 }
 
 template <int KC>
@@ -1003,12 +1086,12 @@ static long long* g_trace = nullptr;
 long long* dense_conv_trace_buffer() { return g_trace; }
 void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,
                        int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms,
-                       BufDev nxt_acc, BufDev nxt_trunc) {
+                       BufDev nxt_acc, BufDev nxt_trunc, unsigned* tmax) {
     if (!p.ok) throw std::runtime_error("conv_dense: unsupported layer shape");
     DenseArgs a{in, out, w, units, nunits, p.smax > 1 ? ws : nullptr, cnt, cin, cout, p.cout_pad, p.k, p.r,
                 p.KC, p.nCB, p.NBD, p.nNB, p.nstw, p.smax > 1 ? p.smax : 1, num_sms, p.s_c4, p.patch_bytes,
                 p.w_stage, p.acc_cols, p.nbuf, p.nbuf * p.acc_cols, p.umax, p.tpu, p.tsh, p.patch_px, p.npb,
-                p.nmma, nxt_acc, nxt_trunc, nullptr, 0};
+                p.nmma, nxt_acc, nxt_trunc, tmax, nullptr, 0};
     if (getenv("DFX_CONV_DBG") && !g_trace) cudaMalloc(&g_trace, 2048 * 8);
     a.trace = g_trace;
     if (const char* d = getenv("DFX_CONV_DBG")) a.dbg = atoi(d);

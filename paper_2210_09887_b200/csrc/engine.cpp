@@ -195,6 +195,11 @@ class Engine {
         DevArr<float> wdense, wsd;
         DevArr<int> dcnt;
         DevArr<int> units;
+        // fused activation pass 1: this dense conv folds max |trunc + delta| of its
+        // sole consuming activation (layer tm_consumer) into that layer's tile_max;
+        // the activation then runs its commit pass only (tm_fused)
+        int tm_consumer = -1;
+        bool tm_fused = false;
     };
 
     void allocate(int th, int tw);
@@ -524,6 +529,30 @@ void Engine::allocate(int th, int tw) {
             }
         }
     }
+    // activation pass 1 fused into the producing dense conv (an all-thread pass at
+    // the end of the kernel, and the plan's zero fill): stride-1 dense convs whose
+    // sole consumer is a truncation point, 32-channel multiples
+    {
+        // opt-in (DFX_FUSE_TM=1): measured 3-7 % SLOWER end to end on C2 (DESIGN.md §3,
+        // negative results): the conv's extra trunc reads sit on its critical tail
+        const char* fe = getenv("DFX_FUSE_TM");
+        const char* ce = getenv("DFX_TRUNC_COOP");
+        const char* te = getenv("DFX_DENSE_TAU");
+        const bool on = (fe && fe[0] == '1') && !(ce && ce[0] == '1') && !(te && atoi(te) > 1);
+        for (size_t i = 0; on && i < net_.layers.size(); ++i) {
+            const Layer& l = net_.layers[i];
+            LayerRT& rt = lrt_[i];
+            if (l.kind != DFX_CONV || !rt.dense || l.cout % 32 != 0 || rt.dp.NBD % 32 != 0) continue;
+            int cj = -1, ncons = 0;
+            for (size_t j = 0; j < net_.layers.size(); ++j)
+                if (net_.layers[j].in0 == (int)i || net_.layers[j].in1 == (int)i) cj = (int)j, ++ncons;
+            if (ncons != 1) continue;
+            const int k = net_.layers[cj].kind;
+            if (k != DFX_RELU && k != DFX_TRUNCATE && k != DFX_OUTPUT) continue;
+            rt.tm_consumer = cj;
+            lrt_[cj].tm_fused = true;
+        }
+    }
     nclaim_bufs_ = (int)cbufs.size();
     claim_bufs_.alloc(cbufs.size());
     CUDA_CHECK(cudaMemcpy(claim_bufs_.p, cbufs.data(), cbufs.size() * sizeof(ClaimBuf), cudaMemcpyHostToDevice));
@@ -807,9 +836,11 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                     // ~10 % update rate: +3 % over sending sparse 16-px-tile strips to the
                     // gathered kernel with tau = 48; DFX_DENSE_TAU overrides)
                     const int tau = tau_env >= 1 ? tau_env : 1;
+                    unsigned* tm = rt.tm_consumer >= 0 ? tmax + (size_t)rt.tm_consumer * nslots : nullptr;
+                    const BufDev tmb = rt.tm_consumer >= 0 ? lrt_[rt.tm_consumer].aux : BufDev{nullptr, 0, 0};
                     PROF(DFX_FAM_CONV_TARGETS, launch_conv_plan(C, s, rt.dp, a, rt.pkt, rt.halo_geom, rt.units.p,
                                                                 ucounts + idx2, flop_px + idx2, tau, rt.list.p,
-                                                                counts + idx2));
+                                                                counts + idx2, tau == 1 ? tm : nullptr, tmb));
                     if (tau > 1 && l.stride == 1)
                         PROF(DFX_FAM_CONV_MMA, launch_conv_tc(C, s, a, rt.wtc.p, l.cin, rt.cin_pad, l.cout, rt.cout_pad,
                                                               l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom, rt.list.p,
@@ -826,7 +857,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                             na = lrt_[cj].acc, nt = lrt_[cj].aux;
                         PROF(DFX_FAM_CONV_MMA, launch_conv_dense(C, s, rt.dp, a, rt.pkt, rt.wdense.p, l.cin, l.cout,
                                                                  rt.units.p, ucounts + idx2, rt.wsd.p, rt.dcnt.p,
-                                                                 num_sms_, na, nt));
+                                                                 num_sms_, na, nt, tau == 1 ? tm : nullptr));
                     }
                     break;
                 }
@@ -848,6 +879,17 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
             case DFX_RELU:
             case DFX_TRUNCATE:
             case DFX_OUTPUT:
+                if (rt.tm_fused) {
+                    // pass 1 ran in the producing conv: commit (+ halo stash) only
+                    BufDev pf0{nullptr, 0, 0}, pf1{nullptr, 0, 0};
+                    int pj = -1, ncons = 0;
+                    for (size_t j = 0; j < net_.layers.size(); ++j)
+                        if (net_.layers[j].in0 == idx2 || net_.layers[j].in1 == idx2) pj = (int)j, ++ncons;
+                    if (ncons == 1 && net_.layers[pj].kind == DFX_MAXPOOL) pf0 = lrt_[pj].acc, pf1 = lrt_[pj].aux;
+                    PROF(DFX_FAM_TRUNC, launch_trunc_commit_stash(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots,
+                                                                  rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt, pf0, pf1));
+                    break;
+                }
                 if (a.halo > 0 && (a.C & 3) != 0) PROF(DFX_FAM_TRUNC, launch_ring_add(C, s, a, rt.aux));
                 {
                     // two streaming passes: tile max (+ the halo stash), then fire / fold (kernels_hbm.cu)

@@ -135,8 +135,10 @@ void dense_conv_prepare_weights(const DenseConvPlan& p, const float* w, int cin,
 // stride-1 conv whose every target is computed by k_conv_dense.
 // Units with >= tau targets go to k_conv_dense, the targets of sparser units
 // to the gathered list (list / lcount) for launch_conv_tc (tau = 1: all dense).
+// tmax / tm_trunc (nullable): fused pass 1 of the consuming activation (see launch_conv_dense).
 void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, int hg, int* units,
-                      int* nunits, unsigned long long* flop_px, int tau, int* list, int* lcount);
+                      int* nunits, unsigned long long* flop_px, int tau, int* list, int* lcount,
+                      unsigned* tmax = nullptr, BufDev tm_trunc = BufDev{nullptr, 0, 0});
 long long* dense_conv_trace_buffer();
 // DFX_KTRACE chain trace: per-translation-unit setters of the stamp buffer
 void ktrace_set_kernels(unsigned long long* b, unsigned* c);
@@ -149,7 +151,13 @@ unsigned long long* trunc_trace_buffer();  // DFX_TRUNC_TRACE: [64 launches][102
 // are prefetched to L2 by the conv), or {nullptr} for none.
 void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,
                        int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms,
-                       BufDev nxt_acc = BufDev{nullptr, 0, 0}, BufDev nxt_trunc = BufDev{nullptr, 0, 0});
+                       BufDev nxt_acc = BufDev{nullptr, 0, 0}, BufDev nxt_trunc = BufDev{nullptr, 0, 0},
+                       unsigned* tmax = nullptr);
+// The consuming activation's pass 2 alone (its pass 1, max |trunc + delta| per
+// tile, was folded into tile_max by the conv: launch_conv_plan / _dense with
+// tmax), plus the halo stash pass 1 used to run. Needs C % 4 == 0.
+void launch_trunc_commit_stash(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
+                               const unsigned* tile_max, float thr, int relu, PktDev out, BufDev pf0, BufDev pf1);
 
 // ---- output (delta_layers.cpp:395-400) ----
 void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out, Readback rb);

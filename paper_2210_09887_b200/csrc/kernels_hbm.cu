@@ -361,11 +361,16 @@ __device__ void commit_body(const Ctx& c, const FrameDev& F, const PktDev& in, B
 
 __global__ void __launch_bounds__(256) k_trunc_commit(Ctx c, PktDev in, BufDev acc, BufDev trunc,
                                                       const unsigned* __restrict__ tile_max, float thr, int relu,
-                                                      PktDev out, BufDev pf0, BufDev pf1) {
+                                                      PktDev out, BufDev pf0, BufDev pf1, int stash) {
     pdl_enter();
     __shared__ int s_list[kMaxList];
     __shared__ int s_warp[8];
     const FrameDev& F = *c.f;
+    // pass 1 ran inside the producing conv: the halo stash (ring slots only,
+    // disjoint from every tile the commit touches) moves here
+    if (stash)
+        ring_add_part(c, F, in, trunc, blockIdx.x * (long long)blockDim.x + threadIdx.x,
+                      (long long)gridDim.x * blockDim.x);
     const int nl = build_tile_list(c, F, in, true, s_list, s_warp);
     commit_body(c, F, in, acc, trunc, tile_max, thr, relu, out, s_list, nl, false, pf0.d ? &pf0 : nullptr,
                 pf1.d ? &pf1 : nullptr);
@@ -620,8 +625,15 @@ int launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, B
     static std::atomic<int> g1_cache[64], g2_cache[64];
     const int g1 = stream_grid(k_trunc_tilemax, g1_cache), g2 = stream_grid(k_trunc_commit, g2_cache);
     launch_pdl(k_trunc_tilemax, g1, 256, 0, s, c, in, trunc, tile_max);
-    launch_pdl(k_trunc_commit, g2, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out, pf0, pf1);
+    launch_pdl(k_trunc_commit, g2, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out, pf0, pf1, 0);
     return 2;
+}
+
+void launch_trunc_commit_stash(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
+                               const unsigned* tile_max, float thr, int relu, PktDev out, BufDev pf0, BufDev pf1) {
+    static std::atomic<int> g_cache[64];
+    const int g = stream_grid(k_trunc_commit, g_cache);
+    launch_pdl(k_trunc_commit, g, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out, pf0, pf1, 1);
 }
 
 bool launch_maxpool_vec(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev prev, int k, PktDev out) {

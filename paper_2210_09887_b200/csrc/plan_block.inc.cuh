@@ -63,6 +63,10 @@ struct PlanArgs {
     int* list;
     int* lcount;
     int tile_units;
+    // fused activation pass 1 (k_conv_dense epilogue): zero-filled pixels of
+    // active placement tiles fold max |trunc| into tile_max here (null: off)
+    unsigned* tile_max;
+    BufDev tm_trunc;
 };
 struct PlanSmem {
     uint32_t bits[4096 / 32];
@@ -72,7 +76,7 @@ struct PlanSmem {
 };
 // One plan block, executed by the NT threads of the calling CTA (the
 // k_conv_plan CTA; NT = threads taking part).
-template <int NT>
+template <int NT, bool TM = false>
 __device__ void plan_block(const Ctx& c, const PlanArgs& pa, int blk, PlanSmem& sm) {
     const PktDev& in = pa.in;
     const PktDev& out = pa.out;
@@ -195,6 +199,26 @@ __device__ void plan_block(const Ctx& c, const PlanArgs& pa, int blk, PlanSmem& 
                     if (src >= 0) {
                         float4* row = reinterpret_cast<float4*>(out.d + pkt_off(out, yy, xx));
                         for (int q = lane & 15; q < C4; q += 16) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                    if (TM) {  // delta is 0 here: max |trunc| of the pixel's channels
+                        const bool in_ext = src >= 0 && yy >= 0 && yy < eh && xx >= 0 && xx < ew;
+                        float mt = 0.0f;
+                        int key = -1;
+                        if (in_ext) {
+                            const int qy = dt(yy), qx = dt(xx);
+                            const BufDev& tb = pa.tm_trunc;
+                            const float4* tp = reinterpret_cast<const float4*>(
+                                tb.d + (size_t)slot_of(F, c.rows, c.cols, qy, qx) * t * t * C +
+                                ((size_t)(yy - qy * t) * t + (xx - qx * t)) * C);
+                            for (int q = lane & 15; q < C4; q += 16) {
+                                const float4 tv = __ldcg(tp + q);
+                                mt = fmaxf(fmaxf(fmaxf(mt, fabsf(tv.x)), fabsf(tv.y)), fmaxf(fabsf(tv.z), fabsf(tv.w)));
+                            }
+                            key = qy * F.tw + qx;
+                        }
+                        const unsigned grp = __match_any_sync(0xffffffffu, key);
+                        const unsigned mx = __reduce_max_sync(grp, __float_as_uint(mt));
+                        if (key >= 0 && mx != 0u && lane == __ffs(grp) - 1) atomicMax(pa.tile_max + key, mx);
                     }
                 }
             }

@@ -80,3 +80,18 @@ def test_tf32x3_c1_config():
         assert ia == ib
         assert np.array_equal(a.input_mask(), b.input_mask())
         assert float(np.abs(oa - ob).max()) <= tol(oa)
+
+
+def test_fused_activation_pass1_matches_reference(monkeypatch):
+    """DFX_FUSE_TM=1 (opt-in: the consuming activation's tile max folded into
+    the dense conv and the plan's zero fill) keeps every mask / info / ledger
+    bit-exact and values within tolerance on the C2 network at its widths."""
+    monkeypatch.setenv("DFX_FUSE_TM", "1")
+    from oracle import oracle
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    from engines import RefEngine
+    from test_gpu_fullwidth import C2_CFG, c2_crop_sequence, run_tf32_parity
+    spec = netgen.vgg8_net(np.random.default_rng(2210))
+    run_tf32_parity(RefEngine(spec, C2_CFG), CudaEngine(spec, C2_CFG, "tf32x3"), spec, c2_crop_sequence(6),
+                    "c2_crops_fused_tm")
