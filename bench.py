@@ -22,8 +22,9 @@ streams, no collective on the data path (`scaling: weak`).
 
 Other configs (`--config`): c3 (ResNet-18-style, 1280x720, pan (+4,+2)), c4
 (HRNet-W32-style, 256x192 crops, patch-update sequence at `--rate`), c5 (64
-c3 streams partitioned over the ranks). `--sweep` adds the update-rate sweep
-(1-50 %) with frames/s and frame-roofline fraction per point.
+c3 streams partitioned over the ranks). The update-rate sweep (1-50 %, frames/s
+and frame-roofline fraction per point) is part of the c2 / c4 lines
+(`--no-sweep` drops it).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config c2|c3|c4|c5] [--streams S] [--sweep] [--dry-run]
@@ -488,11 +489,11 @@ def run_ours(args):
     roof_us = frame_roofline(kernels)
     per_gpu_fps = value / world
     frame_roof = {"us_per_frame": roof_us, "frames_per_s_per_gpu": 1e6 / roof_us if roof_us else None,
-                  "frac": per_gpu_fps * roof_us / 1e6 / max(1, S) if roof_us else None,
+                  "frac": per_gpu_fps * roof_us / 1e6 if roof_us else None,
                   "update_rate": update_rate,
                   "how": "sum over kernel families of algorithmic work / peak (HBM bytes / measured HBM GB/s, conv "
                          "FLOPs / (TF32 peak / 3)) at the measured update rate; frac = achieved per-GPU frames/s "
-                         "per stream x roofline time"}
+                         "(all its streams) x roofline time per frame"}
     per_rank = [rank_fps]
     if dist:
         obj = [None] * world
@@ -603,12 +604,14 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--rate", type=float, default=0.1, help="c4: fraction of tiles updated per frame")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="add the 1-50%% update-rate sweep")
+    ap.add_argument("--sweep", action="store_true", help="add the 1-50%% update-rate sweep (default for c2 / c4)")
+    ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only (no GPU)")
     ap.add_argument("--streams", type=int, default=1,
                     help="independent camera streams per GPU (one engine each, kernels overlap across streams)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    args.sweep = (args.sweep or args.config in ("c2", "c4")) and not args.no_sweep
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(sys.argv[1:], args.gpus))
     if args.dry_run:

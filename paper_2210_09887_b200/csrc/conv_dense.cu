@@ -34,6 +34,7 @@
 // allows: nbuf), 20 and 22 MMA issuers, 21 weight producer. One unit per work item
 // (umax = 1). The plan (dense_conv_plan) picks NBD = min(Cout, 128) columns per
 // N block, nbuf and nstw to fit 200 KB of shared memory and 512 TMEM columns.
+#include <cuda.h>  // CUtensorMap (the encoder is reached through cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -79,6 +80,29 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
+}
+// TMA: one 3-D box (channels, x, y) of the input packet into shared memory.
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+// mbarrier wait that traps instead of hanging (a malformed TMA would never complete)
+__device__ __forceinline__ void mbar_wait_bounded(uint32_t bar, uint32_t parity) {
+    for (long long it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (it > (1LL << 26)) __trap();
+    }
 }
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
@@ -155,6 +179,7 @@ struct DenseArgs {
     int ppx;               // pixels of one unit's patch
     int npb;               // patch ring depth (raw fp32 patches; the producers split hi / lo)
     int nmma;              // MMA issuer warps (2: K-block pairs alternate, one accumulator each)
+    int tma;               // patches by TMA boxes (64-B pixel rows, SWIZZLE_64B) instead of cp.async
     BufDev nxt_acc, nxt_trunc;  // the consuming activation's state (L2 prefetch of this CTA's tiles), .d = null: none
     unsigned* tmax;        // fused tile max (pass 1 of the consuming activation): max |trunc + delta| per
                            // placement tile, atomicMax on the float bits; null: the activation computes it
@@ -301,9 +326,11 @@ __device__ __forceinline__ void store_cols(uint32_t taddr, const uint32_t* v) {
 }
 
 template <int KC>
-__global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArgs a) {
+__global__ void __launch_bounds__(kDenseThreads, 1)
+    k_conv_dense(Ctx c, DenseArgs a, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bar_full[8], bar_empty[8], bar_pf[kMaxPB], bar_pe[kMaxPB], bar_af[2], bar_ae[2];
+    __shared__ __align__(8) uint64_t bar_full[8], bar_empty[8], bar_pf[kMaxPB], bar_pe[kMaxPB], bar_af[2], bar_ae[2],
+        bar_tma[kMaxPB];
     __shared__ uint32_t tmem_base_sh;
     __shared__ int s_last;
     __shared__ int s_red_it;  // item whose split-K partials this CTA reduces at the end (-1: none)
@@ -346,6 +373,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
         for (int i = 0; i < a.npb; ++i) {
             mbar_init(smem_u32(&bar_pf[i]), 4);
             mbar_init(smem_u32(&bar_pe[i]), 4 * kProdWG);
+            mbar_init(smem_u32(&bar_tma[i]), 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(smem_u32(&bar_af[i]), a.nmma);
@@ -450,6 +478,29 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
             }
         }
     };
+    // TMA staging (16x8-px units, one unit per item): the patch box (KC channels
+    // x (8+2r) x (16+2r) pixels, 64-B pixel rows, SWIZZLE_64B) of channel chunk
+    // cbase is one cp.async.bulk.tensor; samples outside the stored packet come
+    // back zero from the TMA unit itself, samples inside it but outside the grown
+    // extent or in unwritten tiles (s_poff < 0) are zeroed afterwards (fixup).
+    const uint32_t box_bytes = (uint32_t)KC * 4 * PW * (kUY + 2 * a.r);
+    auto tma_chunk = [&](uint32_t buf, int pr, int cbase, uint32_t bar) {
+        const int uv = __ldcg(a.units + UPI * pr);
+        const int y0 = ((uv >> 16) - 1) * kUY - a.r, x0 = ((uv & 0xffff) - 1) * kUX - a.r;
+        mbar_arrive_tx(bar, box_bytes);
+        tma_load_3d(buf, &tmap, cbase, x0 + a.in.halo, y0 + a.in.halo, bar);
+    };
+    auto fixup = [&](uint32_t buf, int t0, int stride) {
+        for (int p = t0; p < P; p += stride)
+            if (s_poff[p] < 0) {
+                const uint32_t d = buf + (uint32_t)p * 64;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(d + 16 * q), "r"(0) : "memory");
+            }
+    };
+    if (a.tma && (sbase & 511u)) __trap();  // the swizzle pattern below assumes 512-B aligned patch buffers
+
     // Prologue: the CTA's first patch (offsets + first channel chunk) is built by
     // ALL threads, so the first MMA is not gated by 4 loader warps walking a
     // dependent chain alone (~4-6 us per launch before).
@@ -469,10 +520,16 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                          smem_u32(&bar_full[i]));
             }
         }
+        if (a.tma && tid == 0) tma_chunk(sbase, pr, (kb0 / K2) * KC, smem_u32(&bar_tma[0]));
         patch_offsets(pr, nu, tid, kDenseThreads);
         __syncthreads();
-        copy_chunk(sbase, (kb0 / K2) * KC, nu, tid, kDenseThreads);
-        cp_async_wait_all();
+        if (a.tma) {
+            mbar_wait_bounded(smem_u32(&bar_tma[0]), 0);
+            fixup(sbase, tid, kDenseThreads);
+        } else {
+            copy_chunk(sbase, (kb0 / K2) * KC, nu, tid, kDenseThreads);
+            cp_async_wait_all();
+        }
         __syncthreads();
         if (tid == 0)
             for (int i = 0; i < 4; ++i) mbar_arrive(smem_u32(&bar_pf[0]));  // the 4 loader-warp arrivals
@@ -504,6 +561,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                     if ((int)(g % kProdWG) != wg) continue;
                     const int ky = tap / a.k, kx = tap - ky * a.k;
                     const uint32_t src0 = patch + (uint32_t)(ky * PW + kx) * a.pstr;
+                    // TMA patches are SWIZZLE_64B: 16-B chunk bits [4:5] ^= address bits [7:8]
+                    // (buffer bases are 512-B aligned, so the relative offset decides)
+                    const uint32_t swz = a.tma ? (((src0 - sbase) >> 7) & 3u) << 4 : 0u;
                     const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + a.a_col0 + st * 2 * a.umax * KC;
                     const long long t_a = clock64();
                     mbar_wait(smem_u32(&bar_empty[st]), q ^ 1);
@@ -519,7 +579,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                             asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
                                          : "=r"(hv[4 * q4]), "=r"(hv[4 * q4 + 1]), "=r"(hv[4 * q4 + 2]),
                                            "=r"(hv[4 * q4 + 3])
-                                         : "r"(src + 16 * q4));
+                                         : "r"(src + ((16 * q4) ^ swz)));
 #pragma unroll
                         for (int e = 0; e < KC; ++e) {
                             const float x = __uint_as_float(hv[e]);
@@ -561,8 +621,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_conv_dense(Ctx c, DenseArg
                 if (first && pseq == 0) pseq = 1;
                 const uint32_t pb = pseq % a.npb;
                 mbar_wait(smem_u32(&bar_pe[pb]), ((pseq / a.npb) & 1) ^ 1);
-                copy_chunk(sbase + pb * buf_bytes, cb * KC, nu, lt, 128);
-                cp_async_wait_all();
+                if (a.tma) {
+                    if (lt == 0) tma_chunk(sbase + pb * buf_bytes, pr, cb * KC, smem_u32(&bar_tma[pb]));
+                    mbar_wait_bounded(smem_u32(&bar_tma[pb]), (pseq / a.npb) & 1);
+                    fixup(sbase + pb * buf_bytes, lt, 128);
+                } else {
+                    copy_chunk(sbase + pb * buf_bytes, cb * KC, nu, lt, 128);
+                    cp_async_wait_all();
+                }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bar_pf[pb]));
                 ++pseq;
@@ -958,11 +1024,19 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
         const size_t v = (size_t)atoi(e) * 1024;
         if (v >= 64 * 1024 && v <= 220 * 1024) budget = v;
     }
+    // TMA patch boxes for 16x8-px units with 16-channel K-blocks (64-B pixel rows,
+    // SWIZZLE_64B instead of the cp.async layout's 16-B pad); DFX_DENSE_TMA=0: cp.async
+    const char* te = getenv("DFX_DENSE_TMA");
+    const bool tma_ok = !(te && te[0] == '0') && !p.tpu && cin % 4 == 0;
     auto set_kc = [&](int kc) {
         p.KC = kc;
         p.nCB = p.cin_pad / p.KC;
-        p.s_c4 = (unsigned)p.KC * 4 + 16;  // pixel stride in a patch plane (conflict-free row reads)
-        p.patch_bytes = ((unsigned)p.patch_px * p.s_c4 + 127) / 128 * 128;
+        p.tma = tma_ok && kc == 16;
+        // pixel stride in a patch plane: TMA rows are dense (swizzled); cp.async rows
+        // carry a 16-B pad (conflict-free row reads)
+        p.s_c4 = p.tma ? 64u : (unsigned)p.KC * 4 + 16;
+        p.patch_bytes = p.tma ? ((unsigned)p.patch_px * 64 + 511) / 512 * 512
+                              : ((unsigned)p.patch_px * p.s_c4 + 127) / 128 * 128;
         p.w_stage = (uint32_t)p.NBD * p.KC * 8;
     };
     // raw patches (one fp32 plane each) in a ring of npb buffers: the loaders
@@ -1009,8 +1083,8 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     // benchmarked networks plans 7-8 stages (tools/plan_dump.cpp).
     if (p.nstw < 6) p.ok = false;
     if (getenv("DFX_PLAN_DUMP"))
-        fprintf(stderr, "plan cin=%d cout=%d k=%d t=%d KC=%d nbuf=%d nstw=%d nmma=%d npb=%d tpu=%d ok=%d\n", cin, cout, k,
-                t_out, p.KC, p.nbuf, p.nstw, p.nmma, p.npb, p.tpu, (int)p.ok);
+        fprintf(stderr, "plan cin=%d cout=%d k=%d t=%d KC=%d nbuf=%d nstw=%d nmma=%d npb=%d tpu=%d tma=%d ok=%d\n", cin,
+                cout, k, t_out, p.KC, p.nbuf, p.nstw, p.nmma, p.npb, p.tpu, p.tma, (int)p.ok);
     // units over [-16, rows*t + hg) x [-8, cols*t + hg) (hg <= 8 px of grown halo)
     p.nux_max = (cols * t_out + 8 + kUX - 1) / kUX + 1;
     p.nuy_max = (rows * t_out + 8 + kUY - 1) / kUY + 1;
@@ -1074,24 +1148,49 @@ void launch_conv_plan(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktD
 }
 
 template <int KC>
-static void launch_kc(int grid, size_t smem, cudaStream_t s, const Ctx& c, const DenseArgs& a) {
+static void launch_kc(int grid, size_t smem, cudaStream_t s, const Ctx& c, const DenseArgs& a, const CUtensorMap& tm) {
     static std::atomic<unsigned long long> configured{0};
     once_per_device(configured, [] {
         cudaFuncSetAttribute(k_conv_dense<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     });
-    launch_pdl(k_conv_dense<KC>, grid, kDenseThreads, smem, s, c, a);
+    launch_pdl(k_conv_dense<KC>, grid, kDenseThreads, smem, s, c, a, tm);
+}
+
+bool dense_conv_tensor_map(const DenseConvPlan& p, PktDev in, int rows, void* out) {
+    if (!p.tma || (in.C & 3) != 0) return false;
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode enc = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<Encode>(fn);
+    }();
+    if (!enc) return false;
+    // the packet as a 3-D tensor (channels, x, y) over its whole stored array;
+    // coordinates are packet coordinates + halo (TMA fills outside with zeros)
+    const cuuint64_t dims[3] = {(cuuint64_t)in.C, (cuuint64_t)in.pitch_w, (cuuint64_t)(rows * in.t + 2 * in.halo)};
+    const cuuint64_t strides[2] = {(cuuint64_t)in.C * 4, (cuuint64_t)in.pitch_w * in.C * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)p.KC, (cuuint32_t)(kUX + 2 * p.r), (cuuint32_t)(kUY + 2 * p.r)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, in.d, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 static long long* g_trace = nullptr;
 long long* dense_conv_trace_buffer() { return g_trace; }
 void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,
                        int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms,
-                       BufDev nxt_acc, BufDev nxt_trunc, unsigned* tmax) {
+                       BufDev nxt_acc, BufDev nxt_trunc, unsigned* tmax, const void* tmap) {
     if (!p.ok) throw std::runtime_error("conv_dense: unsupported layer shape");
     DenseArgs a{in, out, w, units, nunits, p.smax > 1 ? ws : nullptr, cnt, cin, cout, p.cout_pad, p.k, p.r,
                 p.KC, p.nCB, p.NBD, p.nNB, p.nstw, p.smax > 1 ? p.smax : 1, num_sms, p.s_c4, p.patch_bytes,
                 p.w_stage, p.acc_cols, p.nbuf, p.nbuf * p.acc_cols, p.umax, p.tpu, p.tsh, p.patch_px, p.npb,
-                p.nmma, nxt_acc, nxt_trunc, tmax, nullptr, 0};
+                p.nmma, tmap != nullptr ? 1 : 0, nxt_acc, nxt_trunc, tmax, nullptr, 0};
     if (getenv("DFX_CONV_DBG") && !g_trace) cudaMalloc(&g_trace, 2048 * 8);
     a.trace = g_trace;
     if (const char* d = getenv("DFX_CONV_DBG")) a.dbg = atoi(d);
@@ -1107,9 +1206,12 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
     }
     const long long max_items = (long long)p.ws_units * p.nNB * a.smax;
     const int grid = (int)(max_items < num_sms ? (max_items < 1 ? 1 : max_items) : num_sms);
-    if (p.KC == 32) launch_kc<32>(grid, p.smem, s, c, a);
-    else if (p.KC == 16) launch_kc<16>(grid, p.smem, s, c, a);
-    else launch_kc<8>(grid, p.smem, s, c, a);
+    CUtensorMap tm;
+    if (tmap) memcpy(&tm, tmap, sizeof tm);
+    else memset(&tm, 0, sizeof tm);
+    if (p.KC == 32) launch_kc<32>(grid, p.smem, s, c, a, tm);
+    else if (p.KC == 16) launch_kc<16>(grid, p.smem, s, c, a, tm);
+    else launch_kc<8>(grid, p.smem, s, c, a, tm);
     // split-K partials are reduced inside k_conv_dense (last-arriving CTA)
 }
 

@@ -200,6 +200,9 @@ class Engine {
         // the activation then runs its commit pass only (tm_fused)
         int tm_consumer = -1;
         bool tm_fused = false;
+        // TMA descriptor (CUtensorMap) of the input packet for the patch boxes
+        alignas(64) unsigned char tmap[128];
+        bool has_tmap = false;
     };
 
     void allocate(int th, int tw);
@@ -450,6 +453,8 @@ void Engine::allocate(int th, int tw) {
                         rt.dp = dense_conv_plan(l.cin, l.cout, l.k, l.tile, rows_, cols_, (size_t)256 << 20);
                         rt.dense = rt.dp.ok;
                     }
+                    if (rt.dense && rt.dp.tma)
+                        rt.has_tmap = dense_conv_tensor_map(rt.dp, in_packet(l.in0), rows_, rt.tmap);
                     if (rt.dense) {
                         std::vector<float> wd(dense_conv_weight_floats(rt.dp));
                         dense_conv_prepare_weights(rt.dp, l.w.data(), l.cin, l.cout, wd.data());
@@ -857,7 +862,8 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                             na = lrt_[cj].acc, nt = lrt_[cj].aux;
                         PROF(DFX_FAM_CONV_MMA, launch_conv_dense(C, s, rt.dp, a, rt.pkt, rt.wdense.p, l.cin, l.cout,
                                                                  rt.units.p, ucounts + idx2, rt.wsd.p, rt.dcnt.p,
-                                                                 num_sms_, na, nt, tau == 1 ? tm : nullptr));
+                                                                 num_sms_, na, nt, tau == 1 ? tm : nullptr,
+                                                                 rt.has_tmap ? rt.tmap : nullptr));
                     }
                     break;
                 }

@@ -125,6 +125,7 @@ struct DenseConvPlan {
     int npb;       // patch ring depth
     int nmma;      // MMA issuer warps (1 or 2)
     int ws_units;  // max 128-row units of a frame (split-K workspace rows / 128)
+    int tma;       // 16x8-px units, KC = 16: patches staged by TMA tensor-map boxes (SWIZZLE_64B)
     unsigned s_c4, patch_bytes, w_stage, acc_cols, nbuf;
     size_t smem;
 };
@@ -149,10 +150,14 @@ unsigned long long* frame_trace_host();  // DFX_FRAME_TRACE: [64][4] frame-bound
 unsigned long long* trunc_trace_buffer();  // DFX_TRUNC_TRACE: [64 launches][1024 CTAs][8] globaltimer stamps  // microbenchmark stamps (DFX_CONV_DBG & 64)
 // nxt_acc / nxt_trunc: the consuming activation layer's state buffers (its tiles
 // are prefetched to L2 by the conv), or {nullptr} for none.
+// TMA descriptor of a conv's input packet for the patch boxes of plan p
+// (cuTensorMapEncodeTiled through the runtime's driver entry point); `out` is
+// a CUtensorMap (64 B, 64-B aligned). False: no TMA (the cp.async path runs).
+bool dense_conv_tensor_map(const DenseConvPlan& p, PktDev in, int rows, void* out);
 void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, PktDev in, PktDev out, const float* w,
                        int cin, int cout, const int* units, const int* nunits, float* ws, int* cnt, int num_sms,
                        BufDev nxt_acc = BufDev{nullptr, 0, 0}, BufDev nxt_trunc = BufDev{nullptr, 0, 0},
-                       unsigned* tmax = nullptr);
+                       unsigned* tmax = nullptr, const void* tmap = nullptr);
 // The consuming activation's pass 2 alone (its pass 1, max |trunc + delta| per
 // tile, was folded into tile_max by the conv: launch_conv_plan / _dense with
 // tmax), plus the halo stash pass 1 used to run. Needs C % 4 == 0.
