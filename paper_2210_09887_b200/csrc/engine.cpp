@@ -200,6 +200,10 @@ class Engine {
         // the activation then runs its commit pass only (tm_fused)
         int tm_consumer = -1;
         bool tm_fused = false;
+        // activation pass 2 fused with its sole consuming 2x2 max pool (layer
+        // pool_consumer), which then launches nothing (pool_fused)
+        int pool_consumer = -1;
+        bool pool_fused = false;
         // TMA descriptor (CUtensorMap) of the input packet for the patch boxes
         alignas(64) unsigned char tmap[128];
         bool has_tmap = false;
@@ -558,6 +562,26 @@ void Engine::allocate(int th, int tw) {
             lrt_[cj].tm_fused = true;
         }
     }
+    // activation commit fused with its sole consuming 2x2 / stride-2 max pool
+    // (tile-local; DFX_FUSE_POOL=0 keeps the separate pool launch)
+    {
+        const char* pe = getenv("DFX_FUSE_POOL");
+        const char* ce = getenv("DFX_TRUNC_COOP");
+        const bool on = !(pe && pe[0] == '0') && !(ce && ce[0] == '1');
+        for (size_t i = 0; on && i < net_.layers.size(); ++i) {
+            const Layer& l = net_.layers[i];
+            LayerRT& rt = lrt_[i];
+            if ((l.kind != DFX_RELU && l.kind != DFX_TRUNCATE) || rt.tm_fused || (l.in_channels & 3) != 0) continue;
+            int pj = -1, ncons = 0;
+            for (size_t j = 0; j < net_.layers.size(); ++j)
+                if (net_.layers[j].in0 == (int)i || net_.layers[j].in1 == (int)i) pj = (int)j, ++ncons;
+            if (ncons != 1) continue;
+            const Layer& pl = net_.layers[pj];
+            if (pl.kind != DFX_MAXPOOL || pl.pool_k != 2 || pl.pool_s != 2 || (l.in_tile & 1) != 0) continue;
+            rt.pool_consumer = pj;
+            lrt_[pj].pool_fused = true;
+        }
+    }
     nclaim_bufs_ = (int)cbufs.size();
     claim_bufs_.alloc(cbufs.size());
     CUDA_CHECK(cudaMemcpy(claim_bufs_.p, cbufs.data(), cbufs.size() * sizeof(ClaimBuf), cudaMemcpyHostToDevice));
@@ -896,6 +920,16 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                                                                   rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt, pf0, pf1));
                     break;
                 }
+                if (rt.pool_consumer >= 0) {
+                    // pass 1 (tile max + stash), then pass 2 fused with the consuming max pool
+                    LayerRT& pr = lrt_[rt.pool_consumer];
+                    unsigned* tm = tmax + (size_t)idx2 * nslots;
+                    PROF(DFX_FAM_TRUNC, launch_trunc_tilemax(C, s, a, rt.aux, tm));
+                    PROF(DFX_FAM_TRUNC, launch_trunc_commit_pool(C, s, a, rt.acc, rt.aux, tm, rt.thr,
+                                                                 l.kind == DFX_RELU ? 1 : 0, rt.pkt, pr.acc, pr.aux,
+                                                                 pr.pkt));
+                    break;
+                }
                 if (a.halo > 0 && (a.C & 3) != 0) PROF(DFX_FAM_TRUNC, launch_ring_add(C, s, a, rt.aux));
                 {
                     // two streaming passes: tile max (+ the halo stash), then fire / fold (kernels_hbm.cu)
@@ -931,6 +965,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                 }
                 break;
             case DFX_MAXPOOL:
+                if (rt.pool_fused) break;  // ran inside the producing activation's commit
                 if (a.halo == 0 && l.pool_k == l.pool_s && (a.C & 3) == 0) {
                     PROF(DFX_FAM_POOL, launch_maxpool_vec(C, s, a, rt.acc, rt.aux, l.pool_k, rt.pkt));
                 } else if (a.halo == 0 && l.pool_k == l.pool_s) {
@@ -1077,7 +1112,9 @@ void Engine::prof_harvest() {
             case DFX_MAXPOOL: {
                 const double A = inside(a, ea), T2 = (double)a.t * a.t;
                 const double H = a.halo > 0 ? valid_px(a, ea, true) : 0.0;
-                prof_work_[DFX_FAM_POOL] += 4.0 * a.C * (3 * A * T2 + 3 * H + 3 * valid_px(rt.pkt, eo, false));
+                // a pool fused into the activation's commit is timed with the activation
+                prof_work_[rt.pool_fused ? DFX_FAM_TRUNC : DFX_FAM_POOL] +=
+                    4.0 * a.C * (3 * A * T2 + 3 * H + 3 * valid_px(rt.pkt, eo, false));
                 break;
             }
             case DFX_AVGPOOL:

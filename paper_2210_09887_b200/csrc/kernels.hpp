@@ -161,6 +161,13 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
 // The consuming activation's pass 2 alone (its pass 1, max |trunc + delta| per
 // tile, was folded into tile_max by the conv: launch_conv_plan / _dense with
 // tmax), plus the halo stash pass 1 used to run. Needs C % 4 == 0.
+// Activation pass 1 alone (tile max + halo stash; C % 4 == 0).
+void launch_trunc_tilemax(const Ctx& c, cudaStream_t s, PktDev in, BufDev trunc, unsigned* tile_max);
+// Activation pass 2 fused with its sole consumer, a 2x2 / stride-2 max pool
+// (halo-free, C % 4 == 0): the pool layer then launches nothing.
+void launch_trunc_commit_pool(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
+                              const unsigned* tile_max, float thr, int relu, PktDev out, BufDev pacc, BufDev pprev,
+                              PktDev pout);
 void launch_trunc_commit_stash(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
                                const unsigned* tile_max, float thr, int relu, PktDev out, BufDev pf0, BufDev pf1);
 

@@ -376,6 +376,109 @@ __global__ void __launch_bounds__(256) k_trunc_commit(Ctx c, PktDev in, BufDev a
                 pf1.d ? &pf1 : nullptr);
 }
 
+// Pass 2 of the activation fused with its sole consumer, a 2x2 / stride-2 max
+// pool (delta_layers.cpp:149-232 then :234-318). Both are tile-local: a pool
+// output pixel's window lies inside one activation tile (k == stride, halo 0),
+// and the pool's input mask is the activation's fired mask. Work item = (listed
+// tile, pool output row); unfired tiles fold (trunc += delta) their two input
+// rows; fired tiles commit the 2x2 input pixels of each pool output float4 and
+// immediately fold the activation output into the pool state:
+//   act:  cand = trunc + delta; acc' = acc + cand; trunc = 0; o = relu(acc') - relu(acc)
+//   pool: pacc += o; m = max over the window (first-element init, std::max order);
+//         pool out = m - prev; prev = m
+// The activation output packet is still written (its consumers' readers and the
+// parity tests see it), the pool never re-reads it. Same fp32 operations in the
+// same order as the two kernels, so results are identical.
+__global__ void __launch_bounds__(256) k_trunc_commit_pool(Ctx c, PktDev in, BufDev acc, BufDev trunc,
+                                                           const unsigned* __restrict__ tile_max, float thr, int relu,
+                                                           PktDev out, BufDev pacc, BufDev pprev, PktDev pout) {
+    pdl_enter();
+    __shared__ int s_list[kMaxList];
+    __shared__ int s_warp[8];
+    const FrameDev& F = *c.f;
+    const int T = in.t, to = T / 2, C4 = in.C / 4;
+    // output masks of every placement tile: activation out = fired, pool out = the same
+    for (int ti = blockIdx.x * blockDim.x + threadIdx.x; ti < F.th * F.tw; ti += gridDim.x * blockDim.x) {
+        const int tr = ti / F.tw, tc = ti - tr * F.tw;
+        const float tm = __uint_as_float(__ldcg(tile_max + ti));
+        const uint8_t f = (in.ext[ext_idx(in, tr, tc)] && holds_t(c, F, tr, tc) && tm >= thr && tm > 0.0f) ? 1 : 0;
+        out.ext[ext_idx(out, tr, tc)] = f;
+        pout.ext[ext_idx(pout, tr, tc)] = f;
+    }
+    const int nl = build_tile_list(c, F, in, true, s_list, s_warp);
+    const int items = (nl < 0 ? F.th * F.tw : nl) * to;
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int row4 = T * C4;  // float4s per input tile row
+    for (int it = gw; it < items; it += nw) {
+        const int li = it / to, oy = it - li * to;
+        int ti, tr, tc;
+        list_tile(F, s_list, nl, li, ti, tr, tc);
+        if (nl < 0 && (!in.ext[ext_idx(in, tr, tc)] || !holds_t(c, F, tr, tc))) continue;
+        const float tm = __uint_as_float(__ldcg(tile_max + ti));
+        const bool fire = tm >= thr && tm > 0.0f;
+        float4* tb = reinterpret_cast<float4*>(tile_base(c, F, trunc, tr, tc));
+        float4* ab = reinterpret_cast<float4*>(tile_base(c, F, acc, tr, tc));
+        if (!fire) {  // fold both input rows of this output row
+            for (int q = 2 * oy * row4 + lane; q < (2 * oy + 2) * row4; q += 32) {
+                const int yy = q / row4, rem = q - yy * row4;
+                const float4 dv = __ldcg(reinterpret_cast<const float4*>(in.d + pkt_off(in, tr * T + yy, tc * T)) + rem);
+                __stcs(tb + q, add4(__ldcg(tb + q), dv));
+            }
+            continue;
+        }
+        float4* pab = reinterpret_cast<float4*>(tile_base(c, F, pacc, tr, tc));
+        float4* ppb = reinterpret_cast<float4*>(tile_base(c, F, pprev, tr, tc));
+        for (int q = lane; q < to * C4; q += 32) {
+            const int ox = q / C4, c4 = q - ox * C4;
+            size_t e[4];
+            float4 tv[4], dv[4], av[4], pv[4];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {  // all loads of the window in flight first
+                const int iy = 2 * oy + (w >> 1), ix = 2 * ox + (w & 1);
+                e[w] = ((size_t)iy * T + ix) * C4 + c4;
+                tv[w] = __ldcg(tb + e[w]);
+                av[w] = __ldcg(ab + e[w]);
+                pv[w] = __ldcs(pab + e[w]);
+                dv[w] = __ldcg(reinterpret_cast<const float4*>(in.d + pkt_off(in, tr * T + iy, tc * T + ix)) + c4);
+            }
+            float4* pp = ppb + ((size_t)oy * to + ox) * C4 + c4;
+            const float4 prev = __ldcs(pp);
+            float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const int iy = 2 * oy + (w >> 1), ix = 2 * ox + (w & 1);
+                const float4 cd = add4(tv[w], dv[w]);
+                const float4 nv = add4(av[w], cd);
+                float4 o = cd;
+                if (relu) {
+                    o.x = __fsub_rn(fmaxf(nv.x, 0.f), fmaxf(av[w].x, 0.f));
+                    o.y = __fsub_rn(fmaxf(nv.y, 0.f), fmaxf(av[w].y, 0.f));
+                    o.z = __fsub_rn(fmaxf(nv.z, 0.f), fmaxf(av[w].z, 0.f));
+                    o.w = __fsub_rn(fmaxf(nv.w, 0.f), fmaxf(av[w].w, 0.f));
+                }
+                __stcs(ab + e[w], nv);
+                __stcs(tb + e[w], make_float4(0.f, 0.f, 0.f, 0.f));
+                reinterpret_cast<float4*>(out.d + pkt_off(out, tr * T + iy, tc * T + ix))[c4] = o;
+                const float4 v = add4(pv[w], o);  // pool: acc += delta (delta_layers.cpp:253-261)
+                __stcs(pab + e[w], v);
+                if (w == 0) {
+                    m = v;
+                } else {  // std::max(m, v) == (m < v) ? v : m
+                    m.x = m.x < v.x ? v.x : m.x;
+                    m.y = m.y < v.y ? v.y : m.y;
+                    m.z = m.z < v.z ? v.z : m.z;
+                    m.w = m.w < v.w ? v.w : m.w;
+                }
+            }
+            reinterpret_cast<float4*>(pout.d + pkt_off(pout, tr * to + oy, tc * to + ox))[c4] =
+                make_float4(__fsub_rn(m.x, prev.x), __fsub_rn(m.y, prev.y), __fsub_rn(m.z, prev.z),
+                            __fsub_rn(m.w, prev.w));
+            __stcs(pp, m);
+        }
+    }
+}
+
 // Both passes in ONE cooperative persistent launch (every CTA resident): the
 // tile list is built once, and a grid barrier separates the tile maxima from
 // their use, saving a kernel boundary and its latency chain per layer.
@@ -627,6 +730,19 @@ int launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, B
     launch_pdl(k_trunc_tilemax, g1, 256, 0, s, c, in, trunc, tile_max);
     launch_pdl(k_trunc_commit, g2, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out, pf0, pf1, 0);
     return 2;
+}
+
+void launch_trunc_tilemax(const Ctx& c, cudaStream_t s, PktDev in, BufDev trunc, unsigned* tile_max) {
+    static std::atomic<int> g_cache[64];
+    launch_pdl(k_trunc_tilemax, stream_grid(k_trunc_tilemax, g_cache), 256, 0, s, c, in, trunc, tile_max);
+}
+
+void launch_trunc_commit_pool(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
+                              const unsigned* tile_max, float thr, int relu, PktDev out, BufDev pacc, BufDev pprev,
+                              PktDev pout) {
+    static std::atomic<int> g_cache[64];
+    const int g = stream_grid(k_trunc_commit_pool, g_cache);
+    launch_pdl(k_trunc_commit_pool, g, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out, pacc, pprev, pout);
 }
 
 void launch_trunc_commit_stash(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,

@@ -95,3 +95,18 @@ def test_fused_activation_pass1_matches_reference(monkeypatch):
     spec = netgen.vgg8_net(np.random.default_rng(2210))
     run_tf32_parity(RefEngine(spec, C2_CFG), CudaEngine(spec, C2_CFG, "tf32x3"), spec, c2_crop_sequence(6),
                     "c2_crops_fused_tm")
+
+
+def test_reduced_smem_budget_falls_back_to_gathered_conv(monkeypatch):
+    """DFX_DENSE_SMEM_KB=120 squeezes the wide layers' dense plans below 6
+    weight stages, which are marked unsupported (conv_dense.cu dense_conv_plan):
+    those layers must run on the gathered-target kernel with the same results."""
+    monkeypatch.setenv("DFX_DENSE_SMEM_KB", "120")
+    from oracle import oracle
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    from engines import RefEngine
+    from test_gpu_fullwidth import C2_CFG, c2_crop_sequence, run_tf32_parity
+    spec = netgen.vgg8_net(np.random.default_rng(2210))
+    run_tf32_parity(RefEngine(spec, C2_CFG), CudaEngine(spec, C2_CFG, "tf32x3"), spec, c2_crop_sequence(5),
+                    "c2_crops_smem120")
