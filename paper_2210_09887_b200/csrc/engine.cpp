@@ -204,6 +204,10 @@ class Engine {
         // pool_consumer), which then launches nothing (pool_fused)
         int pool_consumer = -1;
         bool pool_fused = false;
+        // the plan of the consuming stride-1 dense conv (layer plan_conv) runs inside
+        // this activation's commit launch (plan_fused on the conv)
+        int plan_conv = -1;
+        bool plan_fused = false;
         // TMA descriptor (CUtensorMap) of the input packet for the patch boxes
         alignas(64) unsigned char tmap[128];
         bool has_tmap = false;
@@ -582,6 +586,32 @@ void Engine::allocate(int th, int tw) {
             lrt_[pj].pool_fused = true;
         }
     }
+    // the next dense conv's plan inside the activation's commit launch (extra
+    // blocks; the input mask comes from the activation's tile maxima);
+    // DFX_FUSE_PLAN=0 keeps the standalone plan launch
+    {
+        const char* fe = getenv("DFX_FUSE_PLAN");
+        const char* te = getenv("DFX_DENSE_TAU");
+        const bool on = !(fe && fe[0] == '0') && !(te && atoi(te) > 1);
+        auto sole = [&](int i) {
+            int cj = -1, ncons = 0;
+            for (size_t j = 0; j < net_.layers.size(); ++j)
+                if (net_.layers[j].in0 == i || net_.layers[j].in1 == i) cj = (int)j, ++ncons;
+            return ncons == 1 ? cj : -1;
+        };
+        for (size_t i = 0; on && i < net_.layers.size(); ++i) {
+            const Layer& l = net_.layers[i];
+            LayerRT& rt = lrt_[i];
+            if ((l.kind != DFX_RELU && l.kind != DFX_TRUNCATE) || rt.tm_fused || (l.in_channels & 3) != 0) continue;
+            const int src = rt.pool_consumer >= 0 ? rt.pool_consumer : (int)i;  // the conv's input layer
+            const int cj = sole(src);
+            if (cj < 0 || net_.layers[cj].kind != DFX_CONV || net_.layers[cj].in1 >= 0) continue;
+            const LayerRT& cr = lrt_[cj];
+            if (!cr.dense || net_.layers[cj].stride != 1 || cr.tm_consumer >= 0) continue;
+            rt.plan_conv = cj;
+            lrt_[cj].plan_fused = true;
+        }
+    }
     nclaim_bufs_ = (int)cbufs.size();
     claim_bufs_.alloc(cbufs.size());
     CUDA_CHECK(cudaMemcpy(claim_bufs_.p, cbufs.data(), cbufs.size() * sizeof(ClaimBuf), cudaMemcpyHostToDevice));
@@ -867,9 +897,10 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                     const int tau = tau_env >= 1 ? tau_env : 1;
                     unsigned* tm = rt.tm_consumer >= 0 ? tmax + (size_t)rt.tm_consumer * nslots : nullptr;
                     const BufDev tmb = rt.tm_consumer >= 0 ? lrt_[rt.tm_consumer].aux : BufDev{nullptr, 0, 0};
-                    PROF(DFX_FAM_CONV_TARGETS, launch_conv_plan(C, s, rt.dp, a, rt.pkt, rt.halo_geom, rt.units.p,
-                                                                ucounts + idx2, flop_px + idx2, tau, rt.list.p,
-                                                                counts + idx2, tau == 1 ? tm : nullptr, tmb));
+                    if (!rt.plan_fused)  // else it ran inside the producing activation's commit launch
+                        PROF(DFX_FAM_CONV_TARGETS, launch_conv_plan(C, s, rt.dp, a, rt.pkt, rt.halo_geom, rt.units.p,
+                                                                    ucounts + idx2, flop_px + idx2, tau, rt.list.p,
+                                                                    counts + idx2, tau == 1 ? tm : nullptr, tmb));
                     if (tau > 1 && l.stride == 1)
                         PROF(DFX_FAM_CONV_MMA, launch_conv_tc(C, s, a, rt.wtc.p, l.cin, rt.cin_pad, l.cout, rt.cout_pad,
                                                               l.k, l.stride, l.k / 2, rt.pkt, rt.halo_geom, rt.list.p,
@@ -918,6 +949,23 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                     if (ncons == 1 && net_.layers[pj].kind == DFX_MAXPOOL) pf0 = lrt_[pj].acc, pf1 = lrt_[pj].aux;
                     PROF(DFX_FAM_TRUNC, launch_trunc_commit_stash(C, s, a, rt.acc, rt.aux, tmax + (size_t)idx2 * nslots,
                                                                   rt.thr, l.kind == DFX_RELU ? 1 : 0, rt.pkt, pf0, pf1));
+                    break;
+                }
+                if (rt.plan_conv >= 0) {
+                    // pass 1 (tile max + stash), then pass 2 (with the fused max pool, if
+                    // any) and the next conv's plan in one launch
+                    const int cj = rt.plan_conv;
+                    LayerRT& cr = lrt_[cj];
+                    const bool pool = rt.pool_consumer >= 0;
+                    LayerRT* pr = pool ? &lrt_[rt.pool_consumer] : nullptr;
+                    unsigned* tm = tmax + (size_t)idx2 * nslots;
+                    PROF(DFX_FAM_TRUNC, launch_trunc_tilemax(C, s, a, rt.aux, tm));
+                    PROF(DFX_FAM_TRUNC,
+                         launch_trunc_commit_plan(C, s, a, rt.acc, rt.aux, tm, rt.thr, l.kind == DFX_RELU ? 1 : 0,
+                                                  rt.pkt, pool ? pr->acc : BufDev{nullptr, 0, 0},
+                                                  pool ? pr->aux : BufDev{nullptr, 0, 0}, pool ? pr->pkt : PktDev{},
+                                                  cr.dp, in_packet(net_.layers[cj].in0), cr.pkt, cr.halo_geom,
+                                                  cr.units.p, ucounts + cj, flop_px + cj, cr.list.p, counts + cj));
                     break;
                 }
                 if (rt.pool_consumer >= 0) {
@@ -1097,7 +1145,8 @@ void Engine::prof_harvest() {
             case DFX_CONV: {
                 const double per_px = 2.0 * l.k * l.k * l.cin * l.cout;
                 prof_work_[DFX_FAM_CONV_MMA] += per_px * (double)fpx[idx];
-                prof_work_[DFX_FAM_CONV_TARGETS] +=
+                // a plan run inside the producing activation's launch is timed with it
+                prof_work_[rt.plan_fused ? DFX_FAM_TRUNC : DFX_FAM_CONV_TARGETS] +=
                     4.0 * l.cout * std::max(0.0, valid_px(rt.pkt, eo, false) - (double)counts[idx]) + 4.0 * counts[idx];
                 break;
             }

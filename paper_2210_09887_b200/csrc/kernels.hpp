@@ -168,6 +168,13 @@ void launch_trunc_tilemax(const Ctx& c, cudaStream_t s, PktDev in, BufDev trunc,
 void launch_trunc_commit_pool(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
                               const unsigned* tile_max, float thr, int relu, PktDev out, BufDev pacc, BufDev pprev,
                               PktDev pout);
+// Activation pass 2 (with its fused 2x2 max pool when pacc.d != null) and the
+// plan of the consuming stride-1 dense conv (plan p, input packet cin = the
+// activation's / pool's output, output packet cout) in one launch.
+void launch_trunc_commit_plan(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
+                              const unsigned* tile_max, float thr, int relu, PktDev out, BufDev pacc, BufDev pprev,
+                              PktDev pout, const DenseConvPlan& p, PktDev cin, PktDev cout, int hg, int* units,
+                              int* nunits, unsigned long long* flop_px, int* list, int* lcount);
 void launch_trunc_commit_stash(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
                                const unsigned* tile_max, float thr, int relu, PktDev out, BufDev pf0, BufDev pf1);
 

@@ -26,6 +26,7 @@ namespace dfx {
 namespace {
 
 #include "output.inc.cuh"
+#include "plan_block.inc.cuh"  // the next conv's plan, run by extra blocks of a commit launch
 
 #ifndef DFX_TRUNC_MINB  // CTAs per SM of k_trunc_coop (measured: 3 -> 80 registers with spills, slower)
 #define DFX_TRUNC_MINB 2
@@ -280,12 +281,13 @@ __global__ void __launch_bounds__(256) k_trunc_tilemax(Ctx c, PktDev in, BufDev 
 __device__ void commit_body(const Ctx& c, const FrameDev& F, const PktDev& in, BufDev acc, BufDev trunc,
                             const unsigned* __restrict__ tile_max, float thr, int relu, const PktDev& out,
                             const int* s_list, int nl, bool ext_by_items = false,
-                            const BufDev* pf0 = nullptr, const BufDev* pf1 = nullptr) {
+                            const BufDev* pf0 = nullptr, const BufDev* pf1 = nullptr, int B = -1, int NB = 0) {
+    if (B < 0) B = blockIdx.x, NB = gridDim.x;  // blocks [0, NB) of the launch do the commit
     const int T = in.t, E4 = T * T * in.C / 4;
     const Div row4(T * in.C / 4), nch((E4 + kChunkF4 - 1) / kChunkF4);
     // output mask = fired tiles (delta_layers.cpp:203-204), every placement tile
     if (!ext_by_items || nl < 0)
-    for (int ti = blockIdx.x * blockDim.x + threadIdx.x; ti < F.th * F.tw; ti += gridDim.x * blockDim.x) {
+    for (int ti = B * blockDim.x + threadIdx.x; ti < F.th * F.tw; ti += NB * blockDim.x) {
         const int tr = ti / F.tw, tc = ti - tr * F.tw;
         const float tm = __uint_as_float(__ldcg(tile_max + ti));
         out.ext[ext_idx(out, tr, tc)] =
@@ -293,7 +295,7 @@ __device__ void commit_body(const Ctx& c, const FrameDev& F, const PktDev& in, B
     }
     const int items = (nl < 0 ? F.th * F.tw : nl) * nch.d;
     const int lane = threadIdx.x & 31;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int gw = (B * blockDim.x + threadIdx.x) >> 5, nw = (NB * blockDim.x) >> 5;
     for (int it = gw; it < items; it += nw) {
         const int li = nch(it), ch = it - li * nch.d;
         int ti, tr, tc;
@@ -389,16 +391,13 @@ __global__ void __launch_bounds__(256) k_trunc_commit(Ctx c, PktDev in, BufDev a
 // The activation output packet is still written (its consumers' readers and the
 // parity tests see it), the pool never re-reads it. Same fp32 operations in the
 // same order as the two kernels, so results are identical.
-__global__ void __launch_bounds__(256) k_trunc_commit_pool(Ctx c, PktDev in, BufDev acc, BufDev trunc,
-                                                           const unsigned* __restrict__ tile_max, float thr, int relu,
-                                                           PktDev out, BufDev pacc, BufDev pprev, PktDev pout) {
-    pdl_enter();
-    __shared__ int s_list[kMaxList];
-    __shared__ int s_warp[8];
+__device__ void commit_pool_body(const Ctx& c, PktDev in, BufDev acc, BufDev trunc, const unsigned* __restrict__ tile_max,
+                                 float thr, int relu, PktDev out, BufDev pacc, BufDev pprev, PktDev pout, int* s_list,
+                                 int* s_warp, int B, int NB) {
     const FrameDev& F = *c.f;
     const int T = in.t, to = T / 2, C4 = in.C / 4;
     // output masks of every placement tile: activation out = fired, pool out = the same
-    for (int ti = blockIdx.x * blockDim.x + threadIdx.x; ti < F.th * F.tw; ti += gridDim.x * blockDim.x) {
+    for (int ti = B * blockDim.x + threadIdx.x; ti < F.th * F.tw; ti += NB * blockDim.x) {
         const int tr = ti / F.tw, tc = ti - tr * F.tw;
         const float tm = __uint_as_float(__ldcg(tile_max + ti));
         const uint8_t f = (in.ext[ext_idx(in, tr, tc)] && holds_t(c, F, tr, tc) && tm >= thr && tm > 0.0f) ? 1 : 0;
@@ -408,7 +407,7 @@ __global__ void __launch_bounds__(256) k_trunc_commit_pool(Ctx c, PktDev in, Buf
     const int nl = build_tile_list(c, F, in, true, s_list, s_warp);
     const int items = (nl < 0 ? F.th * F.tw : nl) * to;
     const int lane = threadIdx.x & 31;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int gw = (B * blockDim.x + threadIdx.x) >> 5, nw = (NB * blockDim.x) >> 5;
     const int row4 = T * C4;  // float4s per input tile row
     for (int it = gw; it < items; it += nw) {
         const int li = it / to, oy = it - li * to;
@@ -476,6 +475,46 @@ __global__ void __launch_bounds__(256) k_trunc_commit_pool(Ctx c, PktDev in, Buf
                             __fsub_rn(m.w, prev.w));
             __stcs(pp, m);
         }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_trunc_commit_pool(Ctx c, PktDev in, BufDev acc, BufDev trunc,
+                                                           const unsigned* __restrict__ tile_max, float thr, int relu,
+                                                           PktDev out, BufDev pacc, BufDev pprev, PktDev pout) {
+    pdl_enter();
+    __shared__ int s_list[kMaxList];
+    __shared__ int s_warp[8];
+    commit_pool_body(c, in, acc, trunc, tile_max, thr, relu, out, pacc, pprev, pout, s_list, s_warp, blockIdx.x,
+                     gridDim.x);
+}
+
+// The activation's commit (optionally with its fused max pool) and the NEXT
+// stride-1 conv's plan in one launch: blocks [0, nplan) run plan blocks whose
+// input mask comes from the activation's tile maxima (MaskSrc), blocks
+// [nplan, nplan + ncommit) run the commit. The two touch disjoint memory (the
+// plan writes the conv's target list, output ext and zero fill; the commit the
+// activation's / pool's state and packets), so no ordering is needed between them.
+template <bool POOL>
+__global__ void __launch_bounds__(256, 2) k_trunc_commit_plan(Ctx c, PktDev in, BufDev acc, BufDev trunc,
+                                                             const unsigned* __restrict__ tile_max, float thr, int relu,
+                                                             PktDev out, BufDev pacc, BufDev pprev, PktDev pout,
+                                                             BufDev pf0, BufDev pf1, PlanArgs pa, int nplan) {
+    pdl_enter();
+    __shared__ int s_list[kMaxList];
+    __shared__ int s_warp[8];
+    __shared__ PlanSmem sm;
+    if ((int)blockIdx.x < nplan) {
+        plan_block<256>(c, pa, blockIdx.x, sm);
+        return;
+    }
+    const int B = blockIdx.x - nplan, NB = gridDim.x - nplan;
+    if (POOL) {
+        commit_pool_body(c, in, acc, trunc, tile_max, thr, relu, out, pacc, pprev, pout, s_list, s_warp, B, NB);
+    } else {
+        const FrameDev& F = *c.f;
+        const int nl = build_tile_list(c, F, in, true, s_list, s_warp);
+        commit_body(c, F, in, acc, trunc, tile_max, thr, relu, out, s_list, nl, false, pf0.d ? &pf0 : nullptr,
+                    pf1.d ? &pf1 : nullptr, B, NB);
     }
 }
 
@@ -743,6 +782,25 @@ void launch_trunc_commit_pool(const Ctx& c, cudaStream_t s, PktDev in, BufDev ac
     static std::atomic<int> g_cache[64];
     const int g = stream_grid(k_trunc_commit_pool, g_cache);
     launch_pdl(k_trunc_commit_pool, g, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out, pacc, pprev, pout);
+}
+
+void launch_trunc_commit_plan(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
+                              const unsigned* tile_max, float thr, int relu, PktDev out, BufDev pacc, BufDev pprev,
+                              PktDev pout, const DenseConvPlan& p, PktDev cin, PktDev cout, int hg, int* units,
+                              int* nunits, unsigned long long* flop_px, int* list, int* lcount) {
+    static std::atomic<int> g0[64], g1[64];
+    const bool pool = pacc.d != nullptr;
+    const int gcommit = pool ? stream_grid(k_trunc_commit_plan<true>, g1) : stream_grid(k_trunc_commit_plan<false>, g0);
+    PlanArgs pa{cin, cout, p.k, p.r, hg, p.nbw, p.nbh * p.nbw, units, nunits, flop_px, 1, list, lcount,
+                p.tpu ? 1 : 0, nullptr, BufDev{nullptr, 0, 0},
+                MaskSrc{in.ext, in.RT, in.ext_pitch, tile_max, thr}};
+    const int nplan = p.nbh * p.nbw;
+    if (pool)
+        launch_pdl(k_trunc_commit_plan<true>, nplan + gcommit, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out,
+                   pacc, pprev, pout, BufDev{nullptr, 0, 0}, BufDev{nullptr, 0, 0}, pa, nplan);
+    else
+        launch_pdl(k_trunc_commit_plan<false>, nplan + gcommit, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out,
+                   pacc, pprev, pout, BufDev{nullptr, 0, 0}, BufDev{nullptr, 0, 0}, pa, nplan);
 }
 
 void launch_trunc_commit_stash(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,

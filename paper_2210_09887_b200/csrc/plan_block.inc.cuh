@@ -28,16 +28,36 @@ __device__ __forceinline__ bool pkt_ok(const PktDev& p, int th, int tw, int y, i
     return p.ext[ext_idx(p, floor_div32(y, p.t), floor_div32(x, p.t))] != 0;
 }
 
+// Source of the conv input's tile mask: the input packet's ext bytes, or -
+// when the plan runs inside the producing activation's commit launch, whose
+// blocks write that ext concurrently - the activation's fire rule evaluated
+// from its tile maxima (delta_layers.cpp:203-204): masked and owned input tile
+// with tile_max >= thr and > 0.
+struct MaskSrc {
+    const uint8_t* act_ext;  // the activation's INPUT packet ext (null: use the conv input's ext)
+    int act_RT, act_pitch;
+    const unsigned* tmax;
+    float thr;
+};
+__device__ __forceinline__ bool tile_masked(const Ctx& c, const PktDev& in, const MaskSrc& ms, int tw, int tr,
+                                            int tc) {
+    if (!ms.act_ext) return in.ext[ext_idx(in, tr, tc)] != 0;
+    const int ti = tr * tw + tc;
+    if (!ms.act_ext[(tr + ms.act_RT) * ms.act_pitch + tc + ms.act_RT] || !c.own[ti]) return false;
+    const float tm = __uint_as_float(__ldcg(ms.tmax + ti));
+    return tm >= ms.thr && tm > 0.0f;
+}
+
 // Target test of a stride-1 window (delta_layers.cpp:34-45, :60-70).
-__device__ __forceinline__ bool is_target_s1(const PktDev& in, int th, int tw, int oy, int ox, int k, int r,
-                                             const FDiv& dt) {
+__device__ __forceinline__ bool is_target_s1(const Ctx& c, const MaskSrc& ms, const PktDev& in, int th, int tw, int oy,
+                                             int ox, int k, int r, const FDiv& dt) {
     const int iy0 = oy - r - in.halo, iy1 = oy - r + k - 1 + in.halo;
     const int ix0 = ox - r - in.halo, ix1 = ox - r + k - 1 + in.halo;
     const int tr0 = max(dt(iy0), 0), tr1 = min(dt(iy1), th - 1);
     const int tc0 = max(dt(ix0), 0), tc1 = min(dt(ix1), tw - 1);
     for (int tr = tr0; tr <= tr1; ++tr)
         for (int tc = tc0; tc <= tc1; ++tc)
-            if (in.ext[ext_idx(in, tr, tc)]) return true;
+            if (tile_masked(c, in, ms, tw, tr, tc)) return true;
     return false;
 }
 
@@ -67,6 +87,7 @@ struct PlanArgs {
     // active placement tiles fold max |trunc| into tile_max here (null: off)
     unsigned* tile_max;
     BufDev tm_trunc;
+    MaskSrc ms;  // zero: the conv input packet's ext is final (standalone k_conv_plan)
 };
 struct PlanSmem {
     uint32_t bits[4096 / 32];
@@ -116,7 +137,7 @@ __device__ void plan_block(const Ctx& c, const PlanArgs& pa, int blk, PlanSmem& 
         if (p < npx) {
             const int ly = dbw(p), lx = p - ly * BW;
             const int y = Y0 + ly, x = X0 + lx;
-            if (y >= -hg && y < eh + hg && x >= -hg && x < ew + hg) tgt = is_target_s1(in, F.th, F.tw, y, x, k, r, din);
+            if (y >= -hg && y < eh + hg && x >= -hg && x < ew + hg) tgt = is_target_s1(c, pa.ms, in, F.th, F.tw, y, x, k, r, din);
             if (tgt) {
                 ++geo;
                 uid = (ly / kUY) * upr + lx / kUX;

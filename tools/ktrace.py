@@ -7,7 +7,7 @@ import numpy as np, torch  # noqa: E402
 import bench, paper_2210_09887_b200 as dfx  # noqa: E402
 from paper_2210_09887_b200 import _capi  # noqa: E402
 N = 12
-spec, cfg, seq = bench.make_workload(N, seed=1000)
+spec, cfg, seq = bench.make_workload(N, seed=1000, config=os.environ.get("KCONFIG", "c2"))
 e = dfx.DeltaEngine(spec, dfx.EngineConfig(**cfg, conv_mode="tf32x3"))
 dev = [torch.from_numpy(f).cuda() for f, _ in seq]
 for k in range(4):
