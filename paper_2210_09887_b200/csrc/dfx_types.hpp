@@ -54,6 +54,15 @@ struct SlotDev {
     int covered;
 };
 
+// One claim of the frame (buffer_manager.cpp:68-81) in the frame parameter
+// block: the global tile and its slot. k_claims zeroes / bias-fills the slot's
+// tiles and records the new owner in the engine's persistent device slot table.
+struct ClaimRec {
+    int64_t tx, ty;
+    int slot;
+    int pad[3];
+};
+
 // Per-frame parameters, uploaded once per frame; kernels read them from
 // device memory so a frame's launch sequence is fixed (CUDA-graph friendly).
 struct FrameDev {

@@ -219,13 +219,12 @@ class Engine {
     void finish_info(dfx_frame_info* info);
     void ensure_staging(int c, int h, int w, bool host_frame);
     PktDev in_packet(int idx) const { return idx == -1 ? in_pkt_ : lrt_[idx].pkt; }
-    Ctx ctx() const { return Ctx{d_frame_, d_slots_, rows_, cols_, d_own_}; }
+    Ctx ctx() const { return Ctx{d_frame_, slots_d_.p, rows_, cols_, d_own_}; }
     void wait_ack(unsigned seq);
     void set_param_slot(int i) {
         uint8_t* b = params_d_.p + (size_t)i * pstride_;
         d_frame_ = reinterpret_cast<FrameDev*>(b);
-        d_slots_ = reinterpret_cast<SlotDev*>(b + off_slots_);
-        d_claims_ = reinterpret_cast<int*>(b + off_claims_);
+        d_claims_ = reinterpret_cast<ClaimRec*>(b + off_claims_);
         d_fresh_ = b + off_fresh_;
         d_own_ = b + off_own_;
     }
@@ -270,10 +269,16 @@ class Engine {
     unsigned pend_in_val_ = 0;
     const unsigned* pend_out_flag_ = nullptr;
     unsigned pend_out_val_ = 0;
-    size_t params_bytes_ = 0, off_slots_ = 0, off_claims_ = 0, off_fresh_ = 0, off_own_ = 0;
+    size_t params_bytes_ = 0, off_claims_ = 0, off_fresh_ = 0, off_own_ = 0;
+    // persistent device slot table (TileLedger slots: owner coord + used): full
+    // upload only after allocation / reset (slots_stale_), else k_claims records
+    // each frame's claims into it, so the per-frame block stays small
+    DevArr<SlotDev> slots_d_;
+    SlotDev* slots_h_ = nullptr;  // pinned staging of the full upload
+    cudaEvent_t slots_ev_ = nullptr;
+    bool slots_stale_ = true;
     FrameDev* d_frame_ = nullptr;
-    SlotDev* d_slots_ = nullptr;
-    int* d_claims_ = nullptr;
+    ClaimRec* d_claims_ = nullptr;
     uint8_t* d_fresh_ = nullptr;
     uint8_t* d_own_ = nullptr;
     int max_claims_ = 0;
@@ -284,6 +289,7 @@ class Engine {
     DevArr<uint8_t> counters_d_;
     size_t cnt_bytes_ = 0, off_dropped_ = 0, off_counts_ = 0, off_ucounts_ = 0, off_gbar_ = 0, off_tmax_ = 0;
     uint8_t* readback_h_ = nullptr;  // pinned: flop_px, dropped, input mask
+    int rb_n1_ = 0, rb_n2_ = 0;      // readback parts (counters, input mask), 16-B multiples
     float *in_h_ = nullptr, *out_h_ = nullptr;  // pinned staging of run_frame's caller buffers
     size_t in_h_n_ = 0, out_h_n_ = 0;
     // output (out_cur_: the buffer this frame's densify writes)
@@ -356,6 +362,8 @@ Engine::~Engine() {
         params_hb_[i] = nullptr;
     }
     if (readback_h_) cudaFreeHost(readback_h_);
+    if (slots_h_) cudaFreeHost(slots_h_);
+    if (slots_ev_) cudaEventDestroy(slots_ev_);
     if (ack_h_) cudaFreeHost(ack_h_);
     if (in_h_) cudaFreeHost(in_h_);
     if (out_h_) cudaFreeHost(out_h_);
@@ -380,7 +388,7 @@ void Engine::build_packet(LayerRT& rt, int C, int t, int halo) {
     p.pitch_w = cols_ * t + 2 * halo;
     p.ext_pitch = cols_ + 2 * p.RT;
     rt.pkt_d.alloc((size_t)(rows_ * t + 2 * halo) * p.pitch_w * C);
-    rt.pkt_ext.alloc((size_t)(rows_ + 2 * p.RT) * p.ext_pitch);
+    rt.pkt_ext.alloc(((size_t)(rows_ + 2 * p.RT) * p.ext_pitch + 15) / 16 * 16);  // 16-B readback copies
     CUDA_CHECK(cudaMemsetAsync(rt.pkt_ext.p, 0, rt.pkt_ext.n, stream_));
     p.d = rt.pkt_d.p;
     p.ext = rt.pkt_ext.p;
@@ -618,11 +626,16 @@ void Engine::allocate(int th, int tw) {
 
     // frame parameter block
     max_claims_ = slots;
-    off_slots_ = (sizeof(FrameDev) + 15) / 16 * 16;
-    off_claims_ = off_slots_ + (size_t)slots * sizeof(SlotDev);
-    off_fresh_ = off_claims_ + (size_t)max_claims_ * sizeof(int);
+    // [FrameDev | fresh bytes | owned bytes | ClaimRec x max]: k_frame_begin
+    // copies only the used prefix (the claims of the frame) over PCIe
+    off_fresh_ = (sizeof(FrameDev) + 15) / 16 * 16;
     off_own_ = off_fresh_ + slots;
-    params_bytes_ = off_own_ + slots;
+    off_claims_ = (off_own_ + slots + 15) / 16 * 16;
+    params_bytes_ = off_claims_ + (size_t)max_claims_ * sizeof(ClaimRec);
+    slots_d_.alloc(slots);
+    CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&slots_h_), (size_t)slots * sizeof(SlotDev), cudaHostAllocDefault));
+    CUDA_CHECK(cudaEventCreateWithFlags(&slots_ev_, cudaEventDisableTiming));
+    slots_stale_ = true;
     // two device slots (alternating per frame) filled by k_frame_begin from two
     // mapped page-locked host blocks
     pstride_ = (params_bytes_ + 255) / 256 * 256;
@@ -651,7 +664,9 @@ void Engine::allocate(int th, int tw) {
     cnt_bytes_ = (off_tmax_ + nl * (size_t)slots * 4 + 15) / 16 * 16;
     counters_d_.alloc(cnt_bytes_);
     CUDA_CHECK(cudaMemset(counters_d_.p, 0, cnt_bytes_));
-    CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&readback_h_), nl * 8 + 8 + slots, cudaHostAllocMapped));
+    rb_n1_ = (int)((nl * 8 + 8 + 15) / 16 * 16);
+    rb_n2_ = (slots + 15) / 16 * 16;
+    CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&readback_h_), rb_n1_ + rb_n2_, cudaHostAllocMapped));
     CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&readback_d_), readback_h_, 0));
 
     const int ot = net_.layers[net_.out_layer].in_tile;
@@ -663,6 +678,7 @@ void Engine::reset() {
     // engine.cpp:93-108
     if (!initialized_) return;
     ledger_.clear();
+    slots_stale_ = true;  // the next frame uploads the whole (re-planned) slot table
     CUDA_CHECK(cudaMemsetAsync(in_acc_d_.p, 0, in_acc_d_.n * 4, stream_));
     CUDA_CHECK(cudaMemsetAsync(in_trunc_d_.p, 0, in_trunc_d_.n * 4, stream_));
     for (auto& rt : lrt_) {
@@ -801,12 +817,23 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     // the host block is free once k_frame_begin of the slot's previous frame consumed it
     wait_ack(pslot_seq_[pslot_]);
     memcpy(params_h_, &F, sizeof F);
-    SlotDev* hs = reinterpret_cast<SlotDev*>(params_h_ + off_slots_);
     const auto& slots = ledger_.slots();
-    for (size_t i = 0; i < slots.size(); ++i)
-        hs[i] = SlotDev{slots[i].coord.tx, slots[i].coord.ty, slots[i].used ? 1 : 0, slots[i].covered ? 1 : 0};
-    int* hc = reinterpret_cast<int*>(params_h_ + off_claims_);
-    for (size_t i = 0; i < plan.claims.size(); ++i) hc[i] = ledger_.slot_index(plan.claims[i].coord);
+    if (slots_stale_) {
+        // first frame / after a reset: the whole slot table, copied on the engine
+        // stream ahead of this frame's kernels (the frame's claims re-record the
+        // same owners); the staging buffer is reused only after its last copy ran
+        CUDA_CHECK(cudaEventSynchronize(slots_ev_));
+        for (size_t i = 0; i < slots.size(); ++i)
+            slots_h_[i] = SlotDev{slots[i].coord.tx, slots[i].coord.ty, slots[i].used ? 1 : 0, 0};
+        CUDA_CHECK(cudaMemcpyAsync(slots_d_.p, slots_h_, slots.size() * sizeof(SlotDev), cudaMemcpyHostToDevice,
+                                   stream_));
+        CUDA_CHECK(cudaEventRecord(slots_ev_, stream_));
+        slots_stale_ = false;
+    }
+    ClaimRec* hc = reinterpret_cast<ClaimRec*>(params_h_ + off_claims_);
+    for (size_t i = 0; i < plan.claims.size(); ++i)
+        hc[i] = ClaimRec{plan.claims[i].coord.tx, plan.claims[i].coord.ty, ledger_.slot_index(plan.claims[i].coord),
+                         {0, 0, 0}};
     uint8_t* hf = params_h_ + off_fresh_;
     memset(hf, 0, (size_t)rows_ * cols_);
     for (const Coord& t : plan.fresh) {
@@ -825,7 +852,8 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     set_param_slot(pslot_);
     std::atomic_thread_fence(std::memory_order_release);
     launches_ = 0;
-    launch_frame_begin(stream_, params_hd_[pslot_], params_d_.p + (size_t)pslot_ * pstride_, pstride_, counters_d_.p,
+    const size_t pbytes = off_claims_ + plan.claims.size() * sizeof(ClaimRec);  // the used prefix (16-B multiple)
+    launch_frame_begin(stream_, params_hd_[pslot_], params_d_.p + (size_t)pslot_ * pstride_, pbytes, counters_d_.p,
                        cnt_bytes_, ack_d_, fseq_, pend_in_flag_, pend_in_val_, begin_ctr_.p);
     ++launches_;
     const Ctx C = ctx();
@@ -840,7 +868,9 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
 
     // claims reset + implicit bias (buffer_manager.cpp:68-89)
     // (the host knows the claim count: frames without claims skip the launch)
-    if (F.nclaims > 0) PROF(DFX_FAM_CLAIMS, launch_claims(C, s, d_claims_, claim_bufs_.p, nclaim_bufs_, max_claims_));
+    if (F.nclaims > 0)
+        PROF(DFX_FAM_CLAIMS,
+             launch_claims(C, s, d_claims_, nullptr, slots_d_.p, claim_bufs_.p, nclaim_bufs_, max_claims_));
 
     // input stage
     static const bool fuse_input = !(getenv("DFX_FUSE_INPUT") && getenv("DFX_FUSE_INPUT")[0] == '0');
@@ -987,8 +1017,8 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                     DenseOut dz{nullptr, Readback{}};
                     if (fuse_out && idx2 == net_.out_layer)
                         dz = DenseOut{out_cur_ ? out_cur_ : out_d_.p,
-                                      Readback{counters_d_.p, (int)(net_.layers.size() * 8 + 8), in_pkt_ext_.p,
-                                               rows_ * cols_, readback_d_, pend_out_flag_, pend_out_val_}};
+                                      Readback{counters_d_.p, rb_n1_, in_pkt_ext_.p,
+                                               rb_n2_, readback_d_, pend_out_flag_, pend_out_val_}};
                     bool dzd = false;
                     // a sole consuming max pool: its acc / prev tiles of every fired tile go to L2
                     BufDev pf0{nullptr, 0, 0}, pf1{nullptr, 0, 0};
@@ -1031,7 +1061,7 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
         }
     }
     const LayerRT& ort = lrt_[net_.out_layer];
-    const Readback rb{counters_d_.p, (int)(net_.layers.size() * 8 + 8), in_pkt_ext_.p, rows_ * cols_, readback_d_,
+    const Readback rb{counters_d_.p, rb_n1_, in_pkt_ext_.p, rb_n2_, readback_d_,
                       pend_out_flag_, pend_out_val_};
     if (!densified) PROF(DFX_FAM_DENSIFY, launch_densify(C, s, ort.acc, ort.aux, out_cur_ ? out_cur_ : out_d_.p, rb));
     CUDA_CHECK(cudaGetLastError());
@@ -1198,7 +1228,7 @@ void Engine::finish_info(dfx_frame_info* out) {
     }
     const uint64_t dropped = *reinterpret_cast<const uint64_t*>(readback_h_ + nl * 8);
     if (dropped) info.dropped_pixels = (int64_t)dropped;
-    const uint8_t* mask = readback_h_ + nl * 8 + 8;
+    const uint8_t* mask = readback_h_ + rb_n1_;
     int cnt = 0;
     for (int i = 0; i < place_.th * place_.tw; ++i) cnt += mask[(i / place_.tw) * in_pkt_.ext_pitch + i % place_.tw] ? 1 : 0;
     info.update_rate = (double)cnt / ((double)place_.th * place_.tw);
@@ -1371,8 +1401,7 @@ void Engine::input_mask(uint8_t* out, size_t cap, int* th, int* tw) const {
     *th = place_.th;
     *tw = place_.tw;
     check(cap >= (size_t)place_.th * place_.tw, "mask buffer too small");
-    const size_t nl = net_.layers.size();
-    const uint8_t* mask = readback_h_ + nl * 8 + 8;
+    const uint8_t* mask = readback_h_ + rb_n1_;
     for (int r = 0; r < place_.th; ++r)
         for (int c = 0; c < place_.tw; ++c) out[r * place_.tw + c] = mask[r * in_pkt_.ext_pitch + c] ? 1 : 0;
 }

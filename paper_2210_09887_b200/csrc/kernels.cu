@@ -580,8 +580,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-__global__ void k_claims(Ctx c, const int* __restrict__ claim_slots, const ClaimBuf* __restrict__ bufs, int nbuf,
-                         int trace) {
+__global__ void k_claims(Ctx c, const ClaimRec* __restrict__ recs, const int* __restrict__ plain_slots,
+                         SlotDev* __restrict__ table, const ClaimBuf* __restrict__ bufs, int nbuf, int trace) {
     const unsigned long long t0 = trace ? gtimer() : 0;
     pdl_enter();
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -592,6 +592,11 @@ __global__ void k_claims(Ctx c, const int* __restrict__ claim_slots, const Claim
     const FrameDev& F = *c.f;
     const int nq = F.nclaims;
     if (nq == 0) return;
+    // the claimed slots' new owners into the persistent slot table (TileLedger
+    // apply_plan, buffer_manager.cpp:68-81): read by every later kernel of the frame
+    if (table)
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += gridDim.x * blockDim.x)
+            table[recs[i].slot] = SlotDev{recs[i].tx, recs[i].ty, 1, 0};
     // the buffer descriptors in shared memory first (one round of loads, not
     // one dependent global load per buffer in the loop below)
     constexpr int kMaxBufs = 128;
@@ -614,7 +619,7 @@ __global__ void k_claims(Ctx c, const int* __restrict__ claim_slots, const Claim
                     const int ch = 4 * (p2 ? (r & (c4 - 1)) : r % c4);
                     v = make_float4(b.fill[ch], b.fill[ch + 1], b.fill[ch + 2], b.fill[ch + 3]);
                 }
-                reinterpret_cast<float4*>(b.d + (size_t)claim_slots[ci] * n)[r] = v;
+                reinterpret_cast<float4*>(b.d + (size_t)(recs ? recs[ci].slot : plain_slots[ci]) * n)[r] = v;
             }
         } else if ((b.C & 3) == 0) {
             const long long n4 = n / 4;
@@ -625,12 +630,12 @@ __global__ void k_claims(Ctx c, const int* __restrict__ claim_slots, const Claim
                     const int ch = (int)((r * 4) % b.C);
                     v = make_float4(b.fill[ch], b.fill[ch + 1], b.fill[ch + 2], b.fill[ch + 3]);
                 }
-                reinterpret_cast<float4*>(b.d + (size_t)claim_slots[ci] * n)[r] = v;
+                reinterpret_cast<float4*>(b.d + (size_t)(recs ? recs[ci].slot : plain_slots[ci]) * n)[r] = v;
             }
         } else {
             for (long long e = tid0; e < (long long)nq * n; e += nthr) {
                 const long long ci = e / n, r = e - ci * n;
-                b.d[(size_t)claim_slots[ci] * n + r] = b.fill ? b.fill[r % b.C] : 0.0f;
+                b.d[(size_t)(recs ? recs[ci].slot : plain_slots[ci]) * n + r] = b.fill ? b.fill[r % b.C] : 0.0f;
             }
         }
     }
@@ -1460,11 +1465,11 @@ void launch_input_apply(const Ctx& c, cudaStream_t s, const float* aligned, cons
     const int nch = chunks_per_tile(acc.t, acc.C);
     launch_pdl(k_input_apply, c.rows * c.cols * nch, kThreads, 0, s, c, aligned, cov, gate, acc, trunc, out, pitch);
 }
-void launch_claims(const Ctx& c, cudaStream_t s, const int* claim_slots, const ClaimBuf* bufs, int nbuf,
-                   int max_claims) {
+void launch_claims(const Ctx& c, cudaStream_t s, const ClaimRec* recs, const int* plain_slots, SlotDev* table,
+                   const ClaimBuf* bufs, int nbuf, int max_claims) {
     if (nbuf <= 0 || max_claims <= 0) return;
     static const int trace = getenv("DFX_FRAME_TRACE") ? 1 : 0;
-    launch_pdl(k_claims, num_sms_cached() * 8, kThreads, 0, s, c, claim_slots, bufs, nbuf, trace);
+    launch_pdl(k_claims, num_sms_cached() * 8, kThreads, 0, s, c, recs, plain_slots, table, bufs, nbuf, trace);
 }
 void launch_ring_add(const Ctx& c, cudaStream_t s, PktDev in, BufDev dst) {
     if (in.halo <= 0) return;

@@ -39,8 +39,10 @@ void launch_input_apply(const Ctx& c, cudaStream_t s, const float* aligned, cons
                         const uint8_t* gate, BufDev acc, BufDev trunc, PktDev out, int canvas_pitch);
 
 // ---- buffer manager (buffer_manager.cpp:68-89, engine.cpp:78-91) ----
-void launch_claims(const Ctx& c, cudaStream_t s, const int* claim_slots, const ClaimBuf* bufs, int nbuf,
-                   int max_claims);
+// Claims of the frame: recs (engine: ClaimRec in the parameter block; their new
+// owners also go into `table`, the persistent slot table) or plain slot indices.
+void launch_claims(const Ctx& c, cudaStream_t s, const ClaimRec* recs, const int* plain_slots, SlotDev* table,
+                   const ClaimBuf* bufs, int nbuf, int max_claims);
 
 // ---- truncation (delta_layers.cpp:149-232) ----
 void launch_ring_add(const Ctx& c, cudaStream_t s, PktDev in, BufDev dst);

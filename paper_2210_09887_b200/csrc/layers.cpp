@@ -427,7 +427,7 @@ int dfx_claim_reset(dfx_layer_ctx* h, const int64_t* coords, int nclaims, dfx_st
         LCHECK(cudaMemcpyAsync(c.cbufs.p, cb.data(), cb.size() * sizeof(dfx::ClaimBuf), cudaMemcpyHostToDevice,
                                c.stream));
         LCHECK(cudaMemcpyAsync(c.params.p, &F, sizeof F, cudaMemcpyHostToDevice, c.stream));
-        dfx::launch_claims(c.ctx(), c.stream, c.claims.p, c.cbufs.p, nstates, nclaims);
+        dfx::launch_claims(c.ctx(), c.stream, nullptr, c.claims.p, nullptr, c.cbufs.p, nstates, nclaims);
         F.nclaims = 0;
         LCHECK(cudaMemcpyAsync(c.params.p, &F, sizeof F, cudaMemcpyHostToDevice, c.stream));
         LCHECK(cudaGetLastError());

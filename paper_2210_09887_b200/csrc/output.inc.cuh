@@ -20,8 +20,18 @@ __device__ __forceinline__ void wait_flag(const unsigned* f, unsigned v) {
 
 // The frame's small readback (per-layer counts, dropped pixels, fired input
 // tiles) written by CTA 0 of the last kernel straight into mapped host memory.
+// 16-B writes when both parts are 16-B multiples (the engine pads them): every
+// PCIe write is a separate transaction, byte stores cost one each.
 __device__ __forceinline__ void frame_readback(const Readback& rb) {
     if (blockIdx.x != 0 || !rb.dst) return;
+    if (((rb.n1 | rb.n2) & 15) == 0) {
+        uint4* d = reinterpret_cast<uint4*>(rb.dst);
+        const uint4* s1 = reinterpret_cast<const uint4*>(rb.src1);
+        const uint4* s2 = reinterpret_cast<const uint4*>(rb.src2);
+        for (int i = threadIdx.x; i < rb.n1 / 16; i += blockDim.x) d[i] = s1[i];
+        for (int i = threadIdx.x; i < rb.n2 / 16; i += blockDim.x) d[rb.n1 / 16 + i] = s2[i];
+        return;
+    }
     for (int i = threadIdx.x; i < rb.n1; i += blockDim.x) rb.dst[i] = rb.src1[i];
     for (int i = threadIdx.x; i < rb.n2; i += blockDim.x) rb.dst[rb.n1 + i] = rb.src2[i];
 }
