@@ -1063,12 +1063,16 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     }
     // prefer double-buffered accumulators with >= 6 weight stages, else a single
     // accumulator buffer with up to 8 stages
+    // DFX_DENSE_MAXST (6..8): experiments with fewer weight stages (a smaller
+    // shared-memory footprint lets the next kernel's CTAs become resident earlier)
+    int maxst = 8;
+    if (const char* e = getenv("DFX_DENSE_MAXST")) maxst = atoi(e) >= 6 && atoi(e) <= 8 ? atoi(e) : 8;
     p.nbuf = 2;
-    p.nstw = 8;
+    p.nstw = maxst;
     while (p.nstw > 6 && !fits(p.nstw, 2)) --p.nstw;
     if (!fits(p.nstw, 2)) {
         p.nbuf = 1;
-        p.nstw = 8;
+        p.nstw = maxst;
         while (p.nstw > 2 && !fits(p.nstw, 1)) --p.nstw;
     }
     p.acc_cols = acc * p.nmma;
