@@ -208,6 +208,13 @@ class Engine {
         // this activation's commit launch (plan_fused on the conv)
         int plan_conv = -1;
         bool plan_fused = false;
+        // branch streams (DFX_BRANCH_STREAMS=1): this layer's stream (0 = the engine
+        // stream), the producer layers on other streams it waits for, and whether a
+        // consumer on another stream waits for this layer's completion event
+        int sid = 0;
+        std::vector<int> waits;
+        bool signal = false, wait_input = false;
+        cudaEvent_t ev = nullptr;
         // TMA descriptor (CUtensorMap) of the input packet for the patch boxes
         alignas(64) unsigned char tmap[128];
         bool has_tmap = false;
@@ -311,6 +318,15 @@ class Engine {
         int fam;
     };
     bool prof_ = false;
+    cudaStream_t prof_s_ = nullptr;  // the stream the current launch goes to (profiling events)
+    // independent branches of the network (HRNet branches, ResNet projection
+    // shortcuts) on side streams joined by events (DFX_BRANCH_STREAMS=1)
+    bool branch_ = false;
+    std::vector<cudaStream_t> bstreams_;
+    bool input_signal_ = false;
+    cudaEvent_t in_ev_ = nullptr;
+    cudaStream_t lstream(int sid) const { return sid == 0 ? stream_ : bstreams_[sid - 1]; }
+    void plan_branches();
     std::vector<ProfEv> prof_pool_;
     size_t prof_used_ = 0;
     double prof_ms_[DFX_FAMILIES] = {};
@@ -362,6 +378,13 @@ Engine::~Engine() {
         params_hb_[i] = nullptr;
     }
     if (readback_h_) cudaFreeHost(readback_h_);
+    for (cudaStream_t st : bstreams_) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+    }
+    for (auto& rt : lrt_)
+        if (rt.ev) cudaEventDestroy(rt.ev);
+    if (in_ev_) cudaEventDestroy(in_ev_);
     if (slots_h_) cudaFreeHost(slots_h_);
     if (slots_ev_) cudaEventDestroy(slots_ev_);
     if (ack_h_) cudaFreeHost(ack_h_);
@@ -671,6 +694,7 @@ void Engine::allocate(int th, int tw) {
 
     const int ot = net_.layers[net_.out_layer].in_tile;
     out_d_.alloc((size_t)net_.layers[net_.out_layer].in_channels * rows_ * ot * cols_ * ot);
+    plan_branches();
     initialized_ = true;
 }
 
@@ -722,11 +746,58 @@ int Engine::prof_begin(int fam) {
     }
     ProfEv& e = prof_pool_[prof_used_];
     e.fam = fam;
-    CUDA_CHECK(cudaEventRecord(e.a, stream_));
+    CUDA_CHECK(cudaEventRecord(e.a, prof_s_ ? prof_s_ : stream_));
     return (int)prof_used_++;
 }
 void Engine::prof_end(int idx) {
-    if (idx >= 0) CUDA_CHECK(cudaEventRecord(prof_pool_[idx].b, stream_));
+    if (idx >= 0) CUDA_CHECK(cudaEventRecord(prof_pool_[idx].b, prof_s_ ? prof_s_ : stream_));
+}
+
+// Branch streams: a layer continues its first input's stream when it is that
+// producer's first consumer in execution order, else it opens a side stream
+// (round robin over three); cross-stream inputs become event waits, and the
+// output layer joins the engine stream (the frame's last kernel and the
+// readback run there). Layers fused into their producer's launch (the pool /
+// plan / tile-max fusions) are sole consumers, so they share its stream.
+void Engine::plan_branches() {
+    const char* e = getenv("DFX_BRANCH_STREAMS");
+    branch_ = e && e[0] == '1';
+    if (!branch_) return;
+    const int nl = (int)net_.layers.size();
+    std::vector<uint8_t> claimed(nl + 1, 0);  // index nl: the network input
+    int next = 0;
+    const int nside = 3;
+    auto sid_of = [&](int p) { return p < 0 ? 0 : lrt_[p].sid; };
+    for (int idx : net_.topo) {
+        const Layer& l = net_.layers[idx];
+        LayerRT& rt = lrt_[idx];
+        const int p = l.in0, key = p < 0 ? nl : p;
+        if (!claimed[key]) {
+            rt.sid = sid_of(p);
+            claimed[key] = 1;
+        } else {
+            rt.sid = 1 + (next++ % nside);
+        }
+        for (int q : {l.in0, l.in1}) {
+            if (q == -2 || sid_of(q) == rt.sid) continue;
+            if (q == -1) {  // the input packet: the input stage's event on the engine stream
+                rt.wait_input = true;
+                input_signal_ = true;
+                continue;
+            }
+            rt.waits.push_back(q);
+            lrt_[q].signal = true;
+        }
+    }
+    if (lrt_[net_.out_layer].sid != 0) lrt_[net_.out_layer].signal = true;
+    for (int i = 0; i < nside; ++i) {
+        cudaStream_t st = nullptr;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        bstreams_.push_back(st);
+    }
+    for (auto& rt : lrt_)
+        if (rt.signal) CUDA_CHECK(cudaEventCreateWithFlags(&rt.ev, cudaEventDisableTiming));
+    if (input_signal_) CUDA_CHECK(cudaEventCreateWithFlags(&in_ev_, cudaEventDisableTiming));
 }
 
 // engine.cpp:184-287 on device.
@@ -909,11 +980,18 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
     }
 
     // layers in topological order (engine.cpp:247-281)
+    if (branch_ && input_signal_) CUDA_CHECK(cudaEventRecord(in_ev_, stream_));
     bool densified = false;  // the output layer's activation launch also densified
     for (int idx2 : net_.topo) {
         const Layer& l = net_.layers[idx2];
         LayerRT& rt = lrt_[idx2];
         const PktDev a = in_packet(l.in0);
+        const cudaStream_t s = branch_ ? lstream(rt.sid) : stream_;  // this layer's stream
+        prof_s_ = s;
+        if (branch_) {
+            for (int q : rt.waits) CUDA_CHECK(cudaStreamWaitEvent(s, lrt_[q].ev, 0));
+            if (rt.wait_input) CUDA_CHECK(cudaStreamWaitEvent(s, in_ev_, 0));
+        }
         switch (l.kind) {
             case DFX_CONV:
                 if (rt.dense) {
@@ -1059,7 +1137,10 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
             case DFX_BATCHNORM: PROF(DFX_FAM_LINEAR, launch_bn(C, s, a, rt.scale.p, rt.pkt)); break;
             case DFX_ADD: PROF(DFX_FAM_LINEAR, launch_add(C, s, a, in_packet(l.in1), rt.pkt)); break;
         }
+        if (branch_ && rt.signal) CUDA_CHECK(cudaEventRecord(rt.ev, s));
     }
+    prof_s_ = stream_;
+    if (branch_ && lrt_[net_.out_layer].sid != 0) CUDA_CHECK(cudaStreamWaitEvent(stream_, lrt_[net_.out_layer].ev, 0));
     const LayerRT& ort = lrt_[net_.out_layer];
     const Readback rb{counters_d_.p, rb_n1_, in_pkt_ext_.p, rb_n2_, readback_d_,
                       pend_out_flag_, pend_out_val_};

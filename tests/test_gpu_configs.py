@@ -52,3 +52,20 @@ def test_c4_hrnet_exact_vs_reference():
     cfg = dict(tile_size=32, mask_dilation=0)
     seq = netgen.patch_update_sequence(np.random.default_rng(78), 3, 128, 96, 4, 0.2, 32, 0, 32)
     compare_engines(RefEngine(spec, cfg), CudaEngine(spec, cfg, "exact"), spec, seq, check_states=True)
+
+
+@pytest.mark.parametrize("net", ["resnet18", "hrnet"])
+def test_branch_streams_exact_vs_reference(monkeypatch, net):
+    """DFX_BRANCH_STREAMS=1: independent branches (HRNet branches and
+    fusions, ResNet projection shortcuts) run on side streams joined by events;
+    every word must stay bit-identical to the reference (exact mode)."""
+    monkeypatch.setenv("DFX_BRANCH_STREAMS", "1")
+    if net == "resnet18":
+        spec = netgen.resnet18_net(np.random.default_rng(2210))
+        cfg = dict(tile_size=32)
+        seq = netgen.pan_sequence(np.random.default_rng(1001), 3, 96, 128, 4, -5, 3)
+    else:
+        spec = netgen.hrnet_w32_net(np.random.default_rng(2210))
+        cfg = dict(tile_size=32, mask_dilation=0)
+        seq = netgen.patch_update_sequence(np.random.default_rng(78), 3, 128, 96, 4, 0.2, 32, 0, 32)
+    compare_engines(RefEngine(spec, cfg), CudaEngine(spec, cfg, "exact"), spec, seq, check_states=True)
