@@ -753,15 +753,16 @@ void Engine::prof_end(int idx) {
     if (idx >= 0) CUDA_CHECK(cudaEventRecord(prof_pool_[idx].b, prof_s_ ? prof_s_ : stream_));
 }
 
-// Branch streams: a layer continues its first input's stream when it is that
+// Branch streams (measured: C4 HRNet +54 %, C3 ResNet-18 +4 %, chains such
+// as C2 unchanged): a layer continues its first input's stream when it is that
 // producer's first consumer in execution order, else it opens a side stream
 // (round robin over three); cross-stream inputs become event waits, and the
 // output layer joins the engine stream (the frame's last kernel and the
 // readback run there). Layers fused into their producer's launch (the pool /
 // plan / tile-max fusions) are sole consumers, so they share its stream.
 void Engine::plan_branches() {
-    const char* e = getenv("DFX_BRANCH_STREAMS");
-    branch_ = e && e[0] == '1';
+    const char* e = getenv("DFX_BRANCH_STREAMS");  // default on; 0 keeps one stream
+    branch_ = !(e && e[0] == '0');
     if (!branch_) return;
     const int nl = (int)net_.layers.size();
     std::vector<uint8_t> claimed(nl + 1, 0);  // index nl: the network input

@@ -56,7 +56,7 @@ def test_c4_hrnet_exact_vs_reference():
 
 @pytest.mark.parametrize("net", ["resnet18", "hrnet"])
 def test_branch_streams_exact_vs_reference(monkeypatch, net):
-    """DFX_BRANCH_STREAMS=1: independent branches (HRNet branches and
+    """DFX_BRANCH_STREAMS (default on): independent branches (HRNet branches and
     fusions, ResNet projection shortcuts) run on side streams joined by events;
     every word must stay bit-identical to the reference (exact mode)."""
     monkeypatch.setenv("DFX_BRANCH_STREAMS", "1")
