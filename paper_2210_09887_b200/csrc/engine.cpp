@@ -767,7 +767,8 @@ void Engine::plan_branches() {
     const int nl = (int)net_.layers.size();
     std::vector<uint8_t> claimed(nl + 1, 0);  // index nl: the network input
     int next = 0;
-    const int nside = 3;
+    int nside = 3;  // DFX_BRANCH_SIDES (1..8): side streams per engine
+    if (const char* ns = getenv("DFX_BRANCH_SIDES")) nside = std::min(8, std::max(1, atoi(ns)));
     auto sid_of = [&](int p) { return p < 0 ? 0 : lrt_[p].sid; };
     for (int idx : net_.topo) {
         const Layer& l = net_.layers[idx];
