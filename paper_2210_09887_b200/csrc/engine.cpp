@@ -753,10 +753,10 @@ void Engine::prof_end(int idx) {
     if (idx >= 0) CUDA_CHECK(cudaEventRecord(prof_pool_[idx].b, prof_s_ ? prof_s_ : stream_));
 }
 
-// Branch streams (measured: C4 HRNet +54 %, C3 ResNet-18 +4 %, chains such
+// Branch streams (measured: C4 HRNet +64 %, C3 ResNet-18 +4 %, chains such
 // as C2 unchanged): a layer continues its first input's stream when it is that
 // producer's first consumer in execution order, else it opens a side stream
-// (round robin over three); cross-stream inputs become event waits, and the
+// (round robin over six); cross-stream inputs become event waits, and the
 // output layer joins the engine stream (the frame's last kernel and the
 // readback run there). Layers fused into their producer's launch (the pool /
 // plan / tile-max fusions) are sole consumers, so they share its stream.
@@ -767,7 +767,7 @@ void Engine::plan_branches() {
     const int nl = (int)net_.layers.size();
     std::vector<uint8_t> claimed(nl + 1, 0);  // index nl: the network input
     int next = 0;
-    int nside = 3;  // DFX_BRANCH_SIDES (1..8): side streams per engine
+    int nside = 6;  // DFX_BRANCH_SIDES (1..8): side streams per engine (C4: 3 -> 6 measured +6 %, 8 = 6)
     if (const char* ns = getenv("DFX_BRANCH_SIDES")) nside = std::min(8, std::max(1, atoi(ns)));
     auto sid_of = [&](int p) { return p < 0 ? 0 : lrt_[p].sid; };
     for (int idx : net_.topo) {
