@@ -1103,6 +1103,10 @@ DenseConvPlan dense_conv_plan(int cin, int cout, int k, int t_out, int rows, int
     p.nbw = (cols * t_out + 8 + BW - 1) / BW + 1;
     p.t_out = t_out;
     p.smax = 8;
+    if (const char* e = getenv("DFX_DENSE_SMAX")) {  // experiments: cap the split-K factor (1, 2, 4, 8)
+        const int v = atoi(e);
+        if (v >= 1 && v <= 8) p.smax = v;
+    }
     while (p.smax > 1 && (size_t)p.smax * p.ws_units * 128 * p.cout_pad * 4 > ws_budget_bytes) p.smax /= 2;
     return p;
 }
