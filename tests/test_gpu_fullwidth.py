@@ -143,10 +143,12 @@ def test_c2_vgg8_full_frame_tf32x3_vs_reference():
 
 
 # single conv layers at every benchmarked dense plan shape (plus the tile-unit
-# widths the C3 / C4 networks use); identity truncation at threshold 0 so the
+# widths the C3 / C4 networks use, and their stride-32 stages' 1-px tiles, which
+# take the gathered-target kernel); identity truncation at threshold 0 so the
 # output IS the conv of the gated input and no tile decision sits at a threshold
 @pytest.mark.parametrize("cin,cout,t", [(64, 128, 8), (128, 128, 8), (128, 256, 4), (256, 256, 4), (256, 256, 2),
-                                        (128, 128, 4), (256, 256, 8), (32, 32, 8), (512, 512, 2), (64, 64, 8)])
+                                        (128, 128, 4), (256, 256, 8), (32, 32, 8), (512, 512, 2), (64, 64, 8),
+                                        (256, 256, 1), (512, 512, 1)])
 def test_single_conv_dense_plans(cin, cout, t):
     rng = np.random.default_rng(100 + cin + cout + t)
     from paper_2210_09887_b200 import NetworkSpec
