@@ -43,6 +43,23 @@ namespace {
 constexpr int kM = 128;      // target pixels per tile (MMA M)
 constexpr int kKC = 32;      // input channels per K-block
 constexpr int kAStage = kM * kKC * 4 * 2;  // hi + lo = 32 KiB
+// K-block geometry. Input-channel counts of 8 or 16 (padded from an RGB frame's
+// 3, say) pack several taps into one 32-channel K-block (tap-major: tpk taps x
+// cin_pad channels) instead of padding every tap to 32 channels; wider inputs
+// take one (32-channel block, tap) per K-block.
+struct KGeom {
+    int tpk;  // taps per K-block (1: channel block outer, tap inner)
+    int nCB;  // channel blocks
+    int nKB;  // K-blocks
+};
+__host__ __device__ __forceinline__ KGeom k_geom(int cin_pad, int k) {
+    const int K2 = k * k;
+    KGeom g;
+    g.tpk = (cin_pad == 8 || cin_pad == 16) ? kKC / cin_pad : 1;
+    g.nCB = g.tpk > 1 ? 1 : (cin_pad + kKC - 1) / kKC;
+    g.nKB = g.tpk > 1 ? (K2 + g.tpk - 1) / g.tpk : K2 * g.nCB;
+    return g;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -189,9 +206,9 @@ __global__ void __launch_bounds__(kThreadsV2, 1) k_conv_tc(Ctx c, ConvArgs a) {
 
     const FrameDev& F = *c.f;
     const int n = *a.count;
-    const int nCB = (a.cin_pad + kKC - 1) / kKC;
+    const KGeom kg = k_geom(a.cin_pad, a.k);
     const int K2 = a.k * a.k;
-    const int nKB = K2 * nCB;
+    const int nKB = kg.nKB;
     const int nNB = (a.cout_pad + 255) / 256;
     const int S = a.splits;
     const int units = ((n + kM - 1) / kM) * nNB * S;
@@ -277,6 +294,19 @@ __global__ void __launch_bounds__(kThreadsV2, 1) k_conv_tc(Ctx c, ConvArgs a) {
             }
         };
         auto gather = [&](float* v) {
+            if (kg.tpk > 1) {  // tpk taps x cin_pad channels of this K-block
+                const int cp = a.cin_pad;
+#pragma unroll
+                for (int q = 0; q < kKC; q += 8) {
+                    const int tap = kb * kg.tpk + q / cp, c0 = q % cp;
+                    const bool ok = tap < K2 && ((vmask >> tap) & 1ull);
+                    const int ky = ok ? tap / a.k : 0, kx = ok ? tap - ky * a.k : 0;
+                    const float* src = ok ? a.in.d + pkt_off(a.in, py * a.s - a.r + ky, px * a.s - a.r + kx) : nullptr;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) v[q + j] = (ok && c0 + j < a.cin) ? __ldg(src + c0 + j) : 0.0f;
+                }
+                return;
+            }
             const int cb = kb / K2, tap = kb - cb * K2;
             const int ky = tap / a.k, kx = tap - ky * a.k;
             const int cbeg = cb * kKC;
@@ -405,8 +435,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1) k_conv_tc(Ctx c, ConvArgs a) {
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(smem_u32(&bar_full[st]), ph);
                 tc_fence_after();
-                const int c0 = (kb / K2) * kKC;
-                const int nsteps = (a.cin_pad - c0) / 8 < 4 ? (a.cin_pad - c0) / 8 : 4;
+                const int c0 = kg.tpk > 1 ? 0 : (kb / K2) * kKC;
+                const int nsteps = kg.tpk > 1 ? 4 : ((a.cin_pad - c0) / 8 < 4 ? (a.cin_pad - c0) / 8 : 4);
                 const uint32_t b_base = smem_base + st * stage_bytes;
                 const uint32_t a_tm = tmem + a_col0 + st * 64;
                 if (elect_one()) {
@@ -458,28 +488,30 @@ uint32_t rna_tf32_host(float x) {
 }  // namespace
 
 size_t conv_tc_weight_floats(int cin_pad, int cout_pad, int k) {
-    const int nCB = (cin_pad + kKC - 1) / kKC;
-    return (size_t)k * k * nCB * kKC * cout_pad * 2;
+    return (size_t)k_geom(cin_pad, k).nKB * kKC * cout_pad * 2;
 }
 
 // Host: O-I-Kh-Kw fp32 weights -> per (N-block, K-block) smem images
 // [hi: 8 chunks x NB rows x 4 ch][lo: same], zero padded.
 void conv_tc_prepare_weights(const float* w, int cin, int cout, int k, int cin_pad, int cout_pad, float* outp) {
-    const int nCB = (cin_pad + kKC - 1) / kKC, K2 = k * k, nKB = K2 * nCB;
+    const KGeom kg = k_geom(cin_pad, k);
+    const int K2 = k * k, nKB = kg.nKB;
     const int nNB = (cout_pad + 255) / 256;
     memset(outp, 0, conv_tc_weight_floats(cin_pad, cout_pad, k) * sizeof(float));
     for (int nb = 0; nb < nNB; ++nb) {
         const int NB = std::min(256, cout_pad - nb * 256);
         float* base = outp + (size_t)nb * 256 * nKB * kKC * 2;
         for (int kb = 0; kb < nKB; ++kb) {
-            const int cb = kb / K2, tap = kb % K2;
+            const int cb = kb / K2;
             float* blob = base + (size_t)kb * NB * kKC * 2;
             for (int nn = 0; nn < NB; ++nn) {
                 const int o = nb * 256 + nn;
                 for (int ci = 0; ci < kKC; ++ci) {
-                    const int i = cb * kKC + ci;
+                    // K row ci of block kb: (tap, channel) = tap-packed or (block channel, one tap)
+                    const int tap = kg.tpk > 1 ? kb * kg.tpk + ci / cin_pad : kb % K2;
+                    const int i = kg.tpk > 1 ? ci % cin_pad : cb * kKC + ci;
                     float x = 0.0f;
-                    if (o < cout && i < cin) x = w[((size_t)o * cin + i) * K2 + tap];
+                    if (o < cout && i < cin && tap < K2) x = w[((size_t)o * cin + i) * K2 + tap];
                     const uint32_t hb = rna_tf32_host(x);
                     float hi;
                     memcpy(&hi, &hb, 4);
@@ -496,7 +528,7 @@ void conv_tc_prepare_weights(const float* w, int cin, int cout, int k, int cin_p
 }
 
 int conv_tc_splits(int max_targets, int cin_pad, int cout_pad, int k, int num_sms) {
-    const int nCB = (cin_pad + kKC - 1) / kKC, nKB = k * k * nCB;
+    const int nKB = k_geom(cin_pad, k).nKB;
     const int nNB = (cout_pad + 255) / 256;
     const long long tiles = (long long)((max_targets + kM - 1) / kM) * nNB;
     // split K when the layer cannot give every SM a tile; keep >= 4 K-blocks per split
