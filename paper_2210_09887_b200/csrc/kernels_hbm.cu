@@ -266,7 +266,11 @@ __device__ void tilemax_body(const Ctx& c, const FrameDev& F, const PktDev& in, 
     }
 }
 
-__global__ void __launch_bounds__(256) k_trunc_tilemax(Ctx c, PktDev in, BufDev trunc, unsigned* __restrict__ tile_max) {
+#ifndef DFX_TILEMAX_MINB  // resident CTAs per SM of the tile-max pass (register cap)
+#define DFX_TILEMAX_MINB 1
+#endif
+__global__ void __launch_bounds__(256, DFX_TILEMAX_MINB)
+    k_trunc_tilemax(Ctx c, PktDev in, BufDev trunc, unsigned* __restrict__ tile_max) {
     pdl_enter();
     __shared__ int s_list[kMaxList];
     __shared__ int s_warp[8];
