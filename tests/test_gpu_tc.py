@@ -97,11 +97,13 @@ def test_fused_activation_pass1_matches_reference(monkeypatch):
                     "c2_crops_fused_tm")
 
 
-def test_reduced_smem_budget_falls_back_to_gathered_conv(monkeypatch):
-    """DFX_DENSE_SMEM_KB=120 squeezes the wide layers' dense plans below 6
-    weight stages, which are marked unsupported (conv_dense.cu dense_conv_plan):
-    those layers must run on the gathered-target kernel with the same results."""
-    monkeypatch.setenv("DFX_DENSE_SMEM_KB", "120")
+@pytest.mark.parametrize("kb", ["120", "64"])
+def test_reduced_smem_budget_plans(monkeypatch, kb):
+    """DFX_DENSE_SMEM_KB squeezes the dense plans: at 120 KB the 128 / 256-channel
+    layers run 4-5 weight stages (conv_dense.cu dense_conv_plan), at 64 KB they
+    no longer fit and fall back to the gathered-target kernel; results must be
+    the same either way."""
+    monkeypatch.setenv("DFX_DENSE_SMEM_KB", kb)
     from oracle import oracle
     if not oracle.ref_available():
         pytest.skip("oracle/_ref not built")
@@ -109,4 +111,4 @@ def test_reduced_smem_budget_falls_back_to_gathered_conv(monkeypatch):
     from test_gpu_fullwidth import C2_CFG, c2_crop_sequence, run_tf32_parity
     spec = netgen.vgg8_net(np.random.default_rng(2210))
     run_tf32_parity(RefEngine(spec, C2_CFG), CudaEngine(spec, C2_CFG, "tf32x3"), spec, c2_crop_sequence(5),
-                    "c2_crops_smem120")
+                    f"c2_crops_smem{kb}")
