@@ -163,6 +163,9 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
 // The consuming activation's pass 2 alone (its pass 1, max |trunc + delta| per
 // tile, was folded into tile_max by the conv: launch_conv_plan / _dense with
 // tmax), plus the halo stash pass 1 used to run. Needs C % 4 == 0.
+// Upper bound on the warp work items of the activation launches that follow
+// (their persistent grids shrink to it); 0 = none. Per host thread.
+void set_trunc_work_hint(long long items);
 // Activation pass 1 alone (tile max + halo stash; C % 4 == 0).
 void launch_trunc_tilemax(const Ctx& c, cudaStream_t s, PktDev in, BufDev trunc, unsigned* tile_max);
 // Activation pass 2 fused with its sole consumer, a 2x2 / stride-2 max pool

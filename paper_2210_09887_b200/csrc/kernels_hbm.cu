@@ -721,6 +721,18 @@ int stream_grid(K kernel, std::atomic<int> (&cache)[64]) {
 static unsigned long long* g_trunc_trace = nullptr;
 unsigned long long* trunc_trace_buffer() { return g_trunc_trace; }
 
+// Work-proportional grids: an upper bound on the warp work items of the next
+// activation launches (placement tiles x chunks, set by the engine per layer);
+// the persistent grids shrink to ceil(items / 8 warps) so small layers leave SMs
+// to concurrent streams / engines. 0: no bound.
+static thread_local long long g_item_hint = 0;
+void set_trunc_work_hint(long long items) { g_item_hint = items; }
+static int capped(int g) {
+    if (g_item_hint <= 0) return g;
+    const long long need = (g_item_hint + 7) / 8;
+    return need < g ? (int)(need < 1 ? 1 : need) : g;
+}
+
 int launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc, unsigned* tile_max,
                            float thr, int relu, PktDev out, unsigned* gbar, const DenseOut* dzp, bool* dz_done,
                            BufDev pf0, BufDev pf1) {
@@ -769,7 +781,7 @@ int launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, B
         cudaGetLastError();  // fall back to two launches
     }
     static std::atomic<int> g1_cache[64], g2_cache[64];
-    const int g1 = stream_grid(k_trunc_tilemax, g1_cache), g2 = stream_grid(k_trunc_commit, g2_cache);
+    const int g1 = capped(stream_grid(k_trunc_tilemax, g1_cache)), g2 = capped(stream_grid(k_trunc_commit, g2_cache));
     launch_pdl(k_trunc_tilemax, g1, 256, 0, s, c, in, trunc, tile_max);
     launch_pdl(k_trunc_commit, g2, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out, pf0, pf1, 0);
     return 2;
@@ -777,14 +789,14 @@ int launch_trunc_two_pass(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, B
 
 void launch_trunc_tilemax(const Ctx& c, cudaStream_t s, PktDev in, BufDev trunc, unsigned* tile_max) {
     static std::atomic<int> g_cache[64];
-    launch_pdl(k_trunc_tilemax, stream_grid(k_trunc_tilemax, g_cache), 256, 0, s, c, in, trunc, tile_max);
+    launch_pdl(k_trunc_tilemax, capped(stream_grid(k_trunc_tilemax, g_cache)), 256, 0, s, c, in, trunc, tile_max);
 }
 
 void launch_trunc_commit_pool(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
                               const unsigned* tile_max, float thr, int relu, PktDev out, BufDev pacc, BufDev pprev,
                               PktDev pout) {
     static std::atomic<int> g_cache[64];
-    const int g = stream_grid(k_trunc_commit_pool, g_cache);
+    const int g = capped(stream_grid(k_trunc_commit_pool, g_cache));
     launch_pdl(k_trunc_commit_pool, g, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out, pacc, pprev, pout);
 }
 
@@ -794,7 +806,8 @@ void launch_trunc_commit_plan(const Ctx& c, cudaStream_t s, PktDev in, BufDev ac
                               int* nunits, unsigned long long* flop_px, int* list, int* lcount) {
     static std::atomic<int> g0[64], g1[64];
     const bool pool = pacc.d != nullptr;
-    const int gcommit = pool ? stream_grid(k_trunc_commit_plan<true>, g1) : stream_grid(k_trunc_commit_plan<false>, g0);
+    const int gcommit =
+        capped(pool ? stream_grid(k_trunc_commit_plan<true>, g1) : stream_grid(k_trunc_commit_plan<false>, g0));
     PlanArgs pa{cin, cout, p.k, p.r, hg, p.nbw, p.nbh * p.nbw, units, nunits, flop_px, 1, list, lcount,
                 p.tpu ? 1 : 0, nullptr, BufDev{nullptr, 0, 0},
                 MaskSrc{in.ext, in.RT, in.ext_pitch, tile_max, thr}};
@@ -810,7 +823,7 @@ void launch_trunc_commit_plan(const Ctx& c, cudaStream_t s, PktDev in, BufDev ac
 void launch_trunc_commit_stash(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, BufDev trunc,
                                const unsigned* tile_max, float thr, int relu, PktDev out, BufDev pf0, BufDev pf1) {
     static std::atomic<int> g_cache[64];
-    const int g = stream_grid(k_trunc_commit, g_cache);
+    const int g = capped(stream_grid(k_trunc_commit, g_cache));
     launch_pdl(k_trunc_commit, g, 256, 0, s, c, in, acc, trunc, tile_max, thr, relu, out, pf0, pf1, 1);
 }
 
