@@ -9,6 +9,8 @@
 // reference's x86-64 build has no FMA (SURVEY §7 hard part 1).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "kernels.hpp"
 #include "pdl.hpp"
 
@@ -1429,13 +1431,15 @@ void launch_align(const Ctx& c, cudaStream_t s, const float* frame, const float*
 void launch_input_tile_a(const Ctx& c, cudaStream_t s, const float* frame, const float* warped, const uint8_t* fp,
                          int C, float* aligned, int pitch, int T, BufDev acc, BufDev trunc, float thr, uint8_t* cov,
                          uint8_t* sig, int direct) {
-    launch_pdl(k_input_tile_a, num_sms_cached() * 8, kThreads, 0, s, c, frame, warped, fp, C, aligned, pitch, T, acc,
-               trunc, thr, cov, sig, direct);
+    // one CTA per canvas tile at most (the placement has <= rows x cols tiles)
+    const int g = std::min(num_sms_cached() * 8, c.rows * c.cols);
+    launch_pdl(k_input_tile_a, g, kThreads, 0, s, c, frame, warped, fp, C, aligned, pitch, T, acc, trunc, thr, cov, sig,
+               direct);
 }
 void launch_input_tile_b(const Ctx& c, cudaStream_t s, const float* aligned, const uint8_t* cov, const uint8_t* sig,
                          const uint8_t* fresh, int dilation, int pitch, BufDev acc, BufDev trunc, PktDev out) {
-    launch_pdl(k_input_tile_b, num_sms_cached() * 8, kThreads, 0, s, c, aligned, cov, sig, fresh, dilation, pitch, acc,
-               trunc, out);
+    const int g = std::min(num_sms_cached() * 8, c.rows * c.cols);
+    launch_pdl(k_input_tile_b, g, kThreads, 0, s, c, aligned, cov, sig, fresh, dilation, pitch, acc, trunc, out);
 }
 void launch_count_dropped(const Ctx& c, cudaStream_t s, const uint8_t* fp, int T, unsigned long long* counter) {
     launch_pdl(k_count_dropped, num_sms_cached() * 4, kThreads, 0, s, c, fp, T, counter);
@@ -1553,7 +1557,10 @@ void launch_conv_exact(const Ctx& c, cudaStream_t s, PktDev in, const float* w, 
 void launch_densify(const Ctx& c, cudaStream_t s, BufDev acc, BufDev trunc, float* out, Readback rb) {
     if ((acc.C & 7) == 0) {
         static const int trace = getenv("DFX_FRAME_TRACE") ? 1 : 0;
-        launch_pdl(k_densify8, num_sms_cached() * 8, kThreads, 0, s, c, acc, trunc, out, trace, rb);
+        // one warp per (8-channel group, output row): at most (C / 8) x rows x t warps
+        const long long warps = (long long)(acc.C / 8) * c.rows * acc.t;
+        const int g = (int)std::min<long long>(num_sms_cached() * 8, std::max<long long>(1, (warps + 7) / 8));
+        launch_pdl(k_densify8, g, kThreads, 0, s, c, acc, trunc, out, trace, rb);
         return;
     }
     launch_pdl(k_densify, persistent_grid((long long)acc.C * c.rows * acc.t * c.cols * acc.t), kThreads, 0, s, c, acc, trunc,
