@@ -208,6 +208,10 @@ class Engine {
         // this activation's commit launch (plan_fused on the conv)
         int plan_conv = -1;
         bool plan_fused = false;
+        // an add whose input `up_in` is a nearest upsample (sole consumer: this add)
+        // samples that upsample's input itself; the upsample launches nothing
+        int up_in = -1;
+        bool up_fused = false;
         // branch streams (DFX_BRANCH_STREAMS=1): this layer's stream (0 = the engine
         // stream), the producer layers on other streams it waits for, and whether a
         // consumer on another stream waits for this layer's completion event
@@ -642,6 +646,24 @@ void Engine::allocate(int th, int tw) {
             if (!cr.dense || net_.layers[cj].stride != 1 || cr.tm_consumer >= 0) continue;
             rt.plan_conv = cj;
             lrt_[cj].plan_fused = true;
+        }
+    }
+    // nearest upsample folded into its sole consuming add (DFX_FUSE_UPSAMPLE=0: off)
+    {
+        const char* ue = getenv("DFX_FUSE_UPSAMPLE");
+        const bool on = !(ue && ue[0] == '0');
+        for (size_t i = 0; on && i < net_.layers.size(); ++i) {
+            const Layer& l = net_.layers[i];
+            if (l.kind != DFX_ADD || (l.in_channels & 3) != 0) continue;
+            for (int q : {l.in1, l.in0}) {
+                if (q < 0 || net_.layers[q].kind != DFX_UPSAMPLE) continue;
+                int ncons = 0;
+                for (const Layer& m : net_.layers) ncons += (m.in0 == q) + (m.in1 == q);
+                if (ncons != 1 || l.in0 == l.in1) continue;
+                lrt_[i].up_in = q;
+                lrt_[q].up_fused = true;
+                break;
+            }
         }
     }
     nclaim_bufs_ = (int)cbufs.size();
@@ -1143,9 +1165,19 @@ void Engine::enqueue(const float* frame_dev, int c, int h, int w, const float* h
                 }
                 break;
             case DFX_AVGPOOL: PROF(DFX_FAM_POOL, launch_avgpool(C, s, a, l.pool_k, l.pool_s, rt.pkt)); break;
-            case DFX_UPSAMPLE: PROF(DFX_FAM_LINEAR, launch_upsample(C, s, a, l.factor, rt.pkt)); break;
+            case DFX_UPSAMPLE:
+                if (!rt.up_fused) PROF(DFX_FAM_LINEAR, launch_upsample(C, s, a, l.factor, rt.pkt));
+                break;
             case DFX_BATCHNORM: PROF(DFX_FAM_LINEAR, launch_bn(C, s, a, rt.scale.p, rt.pkt)); break;
-            case DFX_ADD: PROF(DFX_FAM_LINEAR, launch_add(C, s, a, in_packet(l.in1), rt.pkt)); break;
+            case DFX_ADD:
+                if (rt.up_in >= 0) {  // the upsample input sampled in place (addition commutes exactly)
+                    const Layer& u = net_.layers[rt.up_in];
+                    const int other = rt.up_in == l.in1 ? l.in0 : l.in1;
+                    PROF(DFX_FAM_LINEAR, launch_add(C, s, in_packet(other), in_packet(u.in0), rt.pkt, u.factor));
+                } else {
+                    PROF(DFX_FAM_LINEAR, launch_add(C, s, a, in_packet(l.in1), rt.pkt));
+                }
+                break;
         }
         if (branch_ && rt.signal) CUDA_CHECK(cudaEventRecord(rt.ev, s));
     }
@@ -1298,7 +1330,9 @@ void Engine::prof_harvest() {
                 break;
             }
             default:
-                prof_work_[DFX_FAM_LINEAR] += 4.0 * a.C * (valid_px(a, ea, false) + valid_px(rt.pkt, eo, false));
+                // a folded upsample writes nothing (its add reads the input instead)
+                prof_work_[DFX_FAM_LINEAR] +=
+                    4.0 * a.C * (valid_px(a, ea, false) + (rt.up_fused ? 0.0 : valid_px(rt.pkt, eo, false)));
         }
     }
     {
@@ -1551,12 +1585,28 @@ void Engine::read_packet(const std::string& layer, float* out, size_t cap, int* 
                          uint8_t* mask, size_t mask_cap) {
     check(have_frame_, "no packet for layer " + layer);
     PktDev p;
+    int f = 1;  // an upsample folded into its add: expand its input packet here
     if (layer == "input") {
         p = in_pkt_;
     } else {
         const int i = net_.index_of(layer);
         check(i >= 0, "no packet for layer " + layer);
         p = lrt_[i].pkt;
+        if (lrt_[i].up_fused) {
+            f = net_.layers[i].factor;
+            const PktDev src = in_packet(net_.layers[i].in0);
+            PktDev v = src;  // the upsampled geometry over the input's storage
+            v.t = src.t * f;
+            v.halo = src.halo * f;
+            p.C = v.C;
+            p.t = v.t;
+            p.halo = v.halo;
+            p.RT = src.RT;
+            p.d = src.d;
+            p.ext = src.ext;
+            p.pitch_w = src.pitch_w;
+            p.ext_pitch = src.ext_pitch;
+        }
     }
     const int th = place_.th, tw = place_.tw;
     *c = p.C;
@@ -1566,7 +1616,8 @@ void Engine::read_packet(const std::string& layer, float* out, size_t cap, int* 
     if (!out) return;
     const size_t n = (size_t)p.C * *gh * *gw;
     check(cap >= n && mask_cap >= (size_t)th * tw, "packet buffer too small");
-    const size_t rows_stored = (size_t)rows_ * p.t + 2 * p.halo;
+    const int sh = p.halo / f, st = p.t / f;  // the stored packet's halo / tile (f = 1: the packet itself)
+    const size_t rows_stored = (size_t)rows_ * st + 2 * sh;
     std::vector<float> raw(rows_stored * p.pitch_w * p.C);
     std::vector<uint8_t> ext((size_t)(rows_ + 2 * p.RT) * p.ext_pitch);
     CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -1576,9 +1627,10 @@ void Engine::read_packet(const std::string& layer, float* out, size_t cap, int* 
         for (int x = -p.halo; x < tw * p.t + p.halo; ++x) {
             const int i = (int)floor_div64(y, p.t), j = (int)floor_div64(x, p.t);
             const bool v = ext[(size_t)(i + p.RT) * p.ext_pitch + (j + p.RT)] != 0;
+            const int sy = (int)floor_div64(y, f), sx = (int)floor_div64(x, f);  // delta_layers.cpp:351-363
             for (int ch = 0; ch < p.C; ++ch)
                 out[((size_t)ch * *gh + (y + p.halo)) * *gw + (x + p.halo)] =
-                    v ? raw[((size_t)(y + p.halo) * p.pitch_w + (x + p.halo)) * p.C + ch] : 0.0f;
+                    v ? raw[((size_t)(sy + sh) * p.pitch_w + (sx + sh)) * p.C + ch] : 0.0f;
         }
     for (int r = 0; r < th; ++r)
         for (int cc = 0; cc < tw; ++cc) mask[r * tw + cc] = ext[(size_t)(r + p.RT) * p.ext_pitch + (cc + p.RT)] ? 1 : 0;

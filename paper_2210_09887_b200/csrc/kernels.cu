@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <stdexcept>
 
 #include "kernels.hpp"
 #include "pdl.hpp"
@@ -1330,7 +1331,10 @@ __device__ __forceinline__ bool ext_in_range(const FrameDev& F, const PktDev& p,
 }
 
 // Add: zero-extended sum, mask OR (delta_layers.cpp:378-393).
-__global__ void k_add(Ctx c, PktDev a, PktDev b, PktDev out) {
+// fb > 1: b is the INPUT of a nearest upsample by fb whose only consumer is
+// this add (delta_layers.cpp:351-363 folded in): the upsampled packet (halo and
+// tile x fb, the same tile indices and ext) is sampled on the fly.
+__global__ void k_add(Ctx c, PktDev a, PktDev b, PktDev out, int fb) {
     pdl_enter();
     const FrameDev& F = *c.f;
     int i, j;
@@ -1350,8 +1354,15 @@ __global__ void k_add(Ctx c, PktDev a, PktDev b, PktDev out) {
             const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
             const float4 sa = (va && pkt_valid(a, F.th, F.tw, oy, ox))
                                   ? reinterpret_cast<const float4*>(a.d + pkt_off(a, oy, ox))[c4] : z;
-            const float4 sb = (vb && pkt_valid(b, F.th, F.tw, oy, ox))
-                                  ? reinterpret_cast<const float4*>(b.d + pkt_off(b, oy, ox))[c4] : z;
+            float4 sb = z;
+            if (fb == 1) {
+                if (vb && pkt_valid(b, F.th, F.tw, oy, ox)) sb = reinterpret_cast<const float4*>(b.d + pkt_off(b, oy, ox))[c4];
+            } else {
+                const int hup = b.halo * fb, tup = b.t * fb;
+                if (vb && oy >= -hup && oy < F.th * tup + hup && ox >= -hup && ox < F.tw * tup + hup &&
+                    b.ext[ext_idx(b, floor_div32(oy, tup), floor_div32(ox, tup))])
+                    sb = reinterpret_cast<const float4*>(b.d + pkt_off(b, floor_div32(oy, fb), floor_div32(ox, fb)))[c4];
+            }
             reinterpret_cast<float4*>(out.d + pkt_off(out, oy, ox))[c4] =
                 make_float4(__fadd_rn(sa.x, sb.x), __fadd_rn(sa.y, sb.y), __fadd_rn(sa.z, sb.z), __fadd_rn(sa.w, sb.w));
         }
@@ -1532,8 +1543,9 @@ void launch_upsample(const Ctx& c, cudaStream_t s, PktDev in, int f, PktDev out)
 void launch_bn(const Ctx& c, cudaStream_t s, PktDev in, const float* scale, PktDev out) {
     launch_pdl(k_bn, ext_blocks(c, out), kThreads, 0, s, c, in, scale, out);
 }
-void launch_add(const Ctx& c, cudaStream_t s, PktDev a, PktDev b, PktDev out) {
-    launch_pdl(k_add, ext_blocks(c, out), kThreads, 0, s, c, a, b, out);
+void launch_add(const Ctx& c, cudaStream_t s, PktDev a, PktDev b, PktDev out, int fb) {
+    if (fb > 1 && (out.C & 3) != 0) throw std::runtime_error("add: upsample fusion needs C % 4 == 0");
+    launch_pdl(k_add, ext_blocks(c, out), kThreads, 0, s, c, a, b, out, fb);
 }
 void launch_conv_targets(const Ctx& c, cudaStream_t s, PktDev in, int k, int st, int r, PktDev out, int hg, int* list,
                          int* count, unsigned long long* flop_px, const uint8_t* dense_map, int nux_max) {

@@ -88,7 +88,8 @@ void launch_maxpool_fused(const Ctx& c, cudaStream_t s, PktDev in, BufDev acc, B
 void launch_avgpool(const Ctx& c, cudaStream_t s, PktDev in, int k, int st, PktDev out);
 void launch_upsample(const Ctx& c, cudaStream_t s, PktDev in, int f, PktDev out);
 void launch_bn(const Ctx& c, cudaStream_t s, PktDev in, const float* scale, PktDev out);
-void launch_add(const Ctx& c, cudaStream_t s, PktDev a, PktDev b, PktDev out);
+// fb > 1: b is the input of an upsample-by-fb folded into the add (C % 4 == 0).
+void launch_add(const Ctx& c, cudaStream_t s, PktDev a, PktDev b, PktDev out, int fb = 1);
 
 // ---- conv (delta_layers.cpp:100-147) ----
 // Target compaction: writes the compacted target list (packed (y+H)<<16 | (x+H),
