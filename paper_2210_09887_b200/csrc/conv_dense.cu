@@ -184,7 +184,8 @@ struct DenseArgs {
     unsigned* tmax;        // fused tile max (pass 1 of the consuming activation): max |trunc + delta| per
                            // placement tile, atomicMax on the float bits; null: the activation computes it
     long long* trace;      // microbenchmark (dbg & 64): per-K-block clock64 stamps of CTA 0
-    int dbg;               // microbenchmark knobs (tools/bench_conv.cu): 1 no MMA, 2 no patch, 4 no weights
+    int dbg;               // microbenchmark knobs (tools/conv_trace*.py): 1 no MMA, 2 no patch loads, 4 no
+                           // weights, 8 no A stores, 64 clock stamps (DFX_CONV_DBG, DFX_CONV_TRACE_IDX)
 };
 
 // Work decomposition for n units x nNB N-blocks x nKB K-blocks, chosen on
@@ -396,7 +397,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     }
     const uint32_t tmem = tmem_base_sh;
     const uint32_t sbase = smem_u32(smem);
-    if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) a.trace[500] = clock64();
+    if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) {
+        a.trace[500] = clock64();
+        a.trace[590] = n, a.trace[591] = S, a.trace[592] = items, a.trace[593] = UPI, a.trace[594] = listed;
+    }
     if ((a.dbg & 64) && tid == 0 && blockIdx.x < 400) {  // per-CTA start (after the wait), %globaltimer
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -569,7 +573,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     mbar_wait(smem_u32(&bar_empty[st]), q ^ 1);
                     const long long t_b = clock64();
                     tc_fence_after();
-                    for (int j = 0; j < nu; ++j) {
+                    for (int j = 0; j < nu && !(a.dbg & 8); ++j) {  // dbg & 8: no A stores (microbenchmark)
                         // raw fp32 row -> hi = x with 13 low mantissa bits cleared (exact
                         // TF32), lo = x - hi (exact; the tensor core reads its top 19 bits)
                         uint32_t hv[KC], lv[KC];
@@ -621,7 +625,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 if (first && pseq == 0) pseq = 1;
                 const uint32_t pb = pseq % a.npb;
                 mbar_wait(smem_u32(&bar_pe[pb]), ((pseq / a.npb) & 1) ^ 1);
-                if (a.tma) {
+                if (a.dbg & 2) {  // microbenchmark: no patch loads
+                } else if (a.tma) {
                     if (lt == 0) tma_chunk(sbase + pb * buf_bytes, pr, cb * KC, smem_u32(&bar_tma[pb]));
                     mbar_wait_bounded(smem_u32(&bar_tma[pb]), (pseq / a.npb) & 1);
                     fixup(sbase + pb * buf_bytes, lt, 128);
@@ -668,6 +673,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const uint32_t b = a.nbuf == 2 ? (ui & 1) : 0, ub = a.nbuf == 2 ? (ui >> 1) : ui;
             mbar_wait(smem_u32(&bar_af[b]), ub & 1);
             const long long t_e0 = clock64();
+            if ((a.dbg & 64) && ui == 0 && tid == 128 * kProdWG + 128 && blockIdx.x < 400) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                a.trace[3100 + blockIdx.x] = (long long)t;  // first accumulator ready
+            }
             tc_fence_after();
             for (int j = 0; j < nu; ++j) {
                 const int u = UPI * pr + j;
@@ -845,6 +855,12 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if ((a.dbg & 64) && tid == 0 && blockIdx.x < 400) {  // items done; does this CTA reduce?
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[2100 + blockIdx.x] = (long long)t;
+        a.trace[2600 + blockIdx.x] = s_red_it >= 0 ? 1 : 0;
+    }
     if (s_red_it >= 0) {
         // fixed-order (split 0, 1, ...) sum of the S partials of one (unit group,
         // N-block) tile into the packet: every thread float4 columns of rows, all
@@ -1199,12 +1215,12 @@ void launch_conv_dense(const Ctx& c, cudaStream_t s, const DenseConvPlan& p, Pkt
                 p.KC, p.nCB, p.NBD, p.nNB, p.nstw, p.smax > 1 ? p.smax : 1, num_sms, p.s_c4, p.patch_bytes,
                 p.w_stage, p.acc_cols, p.nbuf, p.nbuf * p.acc_cols, p.umax, p.tpu, p.tsh, p.patch_px, p.npb,
                 p.nmma, tmap != nullptr ? 1 : 0, nxt_acc, nxt_trunc, tmax, nullptr, 0};
-    if (getenv("DFX_CONV_DBG") && !g_trace) cudaMalloc(&g_trace, 2048 * 8);
+    if (getenv("DFX_CONV_DBG") && !g_trace) cudaMalloc(&g_trace, 4096 * 8);
     a.trace = g_trace;
     if (const char* d = getenv("DFX_CONV_DBG")) a.dbg = atoi(d);
     if (const char* d = getenv("DFX_CONV_TRACE_IDX")) {  // trace only the i-th dense launch of every 8
         static int seq = 0;
-        if (seq++ % 8 != atoi(d)) a.dbg &= ~64;
+        if (seq++ % 8 != atoi(d)) a.dbg = 0;  // every debug bit applies to the traced launch only
     }
     DenseConvPlan pp = p;
     if (a.dbg & 128) a.smax = 1;  // microbenchmark: no split-K

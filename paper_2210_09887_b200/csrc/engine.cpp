@@ -1861,7 +1861,7 @@ int dfx_debug_conv_trace(long long* out, int n) {
         long long* t = dfx::dense_conv_trace_buffer();
         dfx::check(t != nullptr, "no trace (set DFX_CONV_DBG=64)");
         cudaDeviceSynchronize();
-        dfx::check(cudaMemcpy(out, t, (size_t)(n < 2048 ? n : 2048) * 8, cudaMemcpyDeviceToHost) == cudaSuccess,
+        dfx::check(cudaMemcpy(out, t, (size_t)(n < 4096 ? n : 4096) * 8, cudaMemcpyDeviceToHost) == cudaSuccess,
                    "trace copy failed");
     });
 }
