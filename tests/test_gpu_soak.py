@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 import netgen
-from engines import CudaEngine, RefEngine
+from engines import CudaEngine, RefEngine, compare_engines
 from oracle import oracle
 from test_gpu_fullwidth import run_tf32_parity
 
@@ -34,3 +34,17 @@ def test_random_wide_networks_vs_reference(seed):
     seq = netgen.pan_sequence(rng, spec.in_channels, h, w, 5, px, py)
     seq = seq + seq[-2::-1][:2]  # pan back over the same world: evicted / re-claimed tiles
     run_tf32_parity(RefEngine(spec, cfg), CudaEngine(spec, cfg, "tf32x3"), spec, seq, f"soak_{seed}")
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_wide_networks_exact_vs_reference(seed):
+    """The same kind of random DAGs in exact mode: every output, packet, mask,
+    ledger slot and state word bit-identical to the reference."""
+    rng = np.random.default_rng(7300 + seed)
+    spec = netgen.random_network(rng, max_channels=64, in_channels=int(rng.integers(1, 4)))
+    t = int(rng.choice([8, 16]))
+    h, w = t * int(rng.integers(4, 8)), t * int(rng.integers(4, 8))
+    cfg = dict(tile_size=t, input_threshold=float(rng.choice([0.05, 0.15])),
+               default_threshold=float(rng.choice([0.01, 0.03])), mask_dilation=int(rng.integers(0, 5)))
+    seq = netgen.pan_sequence(rng, spec.in_channels, h, w, 5, int(rng.integers(-7, 8)), int(rng.integers(-4, 5)))
+    compare_engines(RefEngine(spec, cfg), CudaEngine(spec, cfg, "exact"), spec, seq + seq[-2::-1][:2])
