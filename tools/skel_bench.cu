@@ -234,15 +234,14 @@ int main() {
     run("skeleton + sttm", {3, 2, 2, 8, 1, 0, 1, 128, KB, 0});
     run("MMA only N=128 (no sttm, no weights)", {3, 2, 2, 8, 0, 1, 0, 128, KB, 0});
     run("MMA only N=128 x4", {3, 2, 4, 8, 0, 1, 0, 128, KB, 0});
-    const int ns[3] = {6, 7, 8};
-    const int ps[4] = {2, 3, 4, 6};
     for (int n : {64, 128})
-        for (int st : ns)
-            for (int pr : ps) {
+        for (int st : {6, 8})
+            for (int pr : {2, 3, 4, 6, 8}) {
                 if (pr > st) continue;
                 char name[96];
-                snprintf(name, sizeof name, "full N=%d, %d stages, 2 issuers x%d", n, st, pr);
-                run(name, {3, 2, pr, st, 2, 1, 1, n, KB, 0});
+                snprintf(name, sizeof name, "full N=%d, %d stages, 1 issuer x%d", n, st, pr);
+                run(name, {3, 1, pr, st, 2, 1, 1, n, KB, 0});
             }
+    run("full N=128, 8 stages, 2 issuers x4 (ref)", {3, 2, 4, 8, 2, 1, 1, 128, KB, 0});
     return 0;
 }
