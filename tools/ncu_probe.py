@@ -1,5 +1,5 @@
 """Run the bench workload (C2) for a few frames with nothing else: the target
-command for ncu captures (python tools/ncu_probe.py [frames])."""
+command for ncu captures (python tools/ncu_probe.py [frames] [config])."""
 import os
 import sys
 
@@ -11,7 +11,8 @@ import bench  # noqa: E402
 import paper_2210_09887_b200 as dfx  # noqa: E402
 
 frames = int(sys.argv[1]) if len(sys.argv) > 1 else 8
-spec, cfg, seq = bench.make_workload(frames, seed=1000)
+config = sys.argv[2] if len(sys.argv) > 2 else "c2"
+spec, cfg, seq = bench.make_workload(frames, seed=1000, config=config)
 eng = dfx.DeltaEngine(spec, dfx.EngineConfig(**cfg, conv_mode="tf32x3"))
 dev = [torch.from_numpy(f).cuda() for f, _ in seq]
 for k in range(frames):
